@@ -1,0 +1,157 @@
+/* flowprefill.h -- C ABI of the B200-native preemptible prefill forward pass.
+ *
+ * The reference (FlowPrefill's prefillsim, /root/reference/pkg/src/prefillsim) has no native
+ * code: its "forward pass" is the cost model + discrete-event execution pool. Each entry point
+ * below replaces one piece of that Python surface; the citation names the reference symbol
+ * whose behaviour the call realises on the GPU.
+ *
+ * Conventions
+ *   - every call returns 0 on success or a negative FP_ERR_* code; fp_last_error() returns a
+ *     thread-local message. No C++ exception crosses this boundary.
+ *   - device memory (weights, paged KV pool, task workspaces) is library-owned. Host arrays are
+ *     caller-owned and only borrowed for the duration of a call.
+ *   - one context per device (= one execution pool, prefillsim/engine.py:137-144). All calls come
+ *     from the owning thread except fp_signal(), which is a single store to pinned memory.
+ */
+#ifndef FLOWPREFILL_H
+#define FLOWPREFILL_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP_OK 0
+#define FP_ERR_ARG -1
+#define FP_ERR_CUDA -2
+#define FP_ERR_NOMEM -3
+#define FP_ERR_STATE -4
+#define FP_ERR_UNSUPPORTED -5
+
+/* Preemption granularity: prefillsim/engine.py:43-47 (PreemptionGranularity). */
+#define FP_GRAN_OPERATOR 0
+#define FP_GRAN_LAYER 1
+#define FP_GRAN_CHUNK 2
+#define FP_GRAN_NONE 3
+
+/* Operator kinds of one dense layer, in timeline order: prefillsim/cost_model.py:38-44. */
+#define FP_OP_QKV_PROJ 0
+#define FP_OP_ATTN 1
+#define FP_OP_O_PROJ 2
+#define FP_OP_GATE_UP_PROJ 3
+#define FP_OP_DOWN_PROJ 4
+
+/* Weight tensor ids for fp_weights_load (canonical, unpacked Llama layout, bf16 row-major). */
+#define FP_W_EMBED 0      /* [vocab, hidden] */
+#define FP_W_Q 1          /* [n_heads*head_dim, hidden] */
+#define FP_W_K 2          /* [n_kv_heads*head_dim, hidden] */
+#define FP_W_V 3          /* [n_kv_heads*head_dim, hidden] */
+#define FP_W_O 4          /* [hidden, n_heads*head_dim] */
+#define FP_W_GATE 5       /* [ffn, hidden] */
+#define FP_W_UP 6         /* [ffn, hidden] */
+#define FP_W_DOWN 7       /* [hidden, ffn] */
+#define FP_W_ATTN_NORM 8  /* [hidden] */
+#define FP_W_FFN_NORM 9   /* [hidden] */
+#define FP_W_FINAL_NORM 10 /* [hidden] */
+#define FP_W_LM_HEAD 11   /* [vocab, hidden] */
+
+typedef struct fp_model_cfg {
+  int32_t num_layers; /* CostParams.num_layers, cost_model.py:92 */
+  int32_t hidden;
+  int32_t n_heads;
+  int32_t n_kv_heads;
+  int32_t head_dim; /* must be 128 */
+  int32_t ffn;
+  int32_t vocab;
+  int32_t max_pos; /* RoPE table length */
+  float rope_theta;
+  float rms_eps;
+} fp_model_cfg;
+
+typedef struct fp_ctx fp_ctx;
+typedef struct fp_task fp_task;
+
+/* Control-block snapshot (the ACK half of the handshake, engine.py:240-291). */
+typedef struct fp_status {
+  int32_t ack_seq;        /* bumped once per acknowledged preemption */
+  int32_t ack_task;       /* task that stopped */
+  int32_t ack_entry;      /* new cursor of that task (first entry not executed) */
+  int32_t progress_task;  /* task whose entry most recently passed its boundary check */
+  int32_t progress_entry;
+  int32_t signal;         /* pending preemption signal (1) or none (0) */
+  uint64_t ack_ns;        /* device %globaltimer at the stop decision */
+} fp_status;
+
+/* Task execution state (TaskState, engine.py:36-40). */
+#define FP_TASK_IDLE 0
+#define FP_TASK_RUNNING 1
+#define FP_TASK_STOPPED 2
+#define FP_TASK_DONE 3
+typedef struct fp_task_status {
+  int32_t state;
+  int32_t cursor;     /* entries [0, cursor) are complete */
+  int32_t generation; /* bumped per submit/resume segment (engine.py:286) */
+  int32_t enqueued;   /* entries handed to the GPU so far in this segment */
+} fp_task_status;
+
+const char* fp_last_error(void);
+int fp_version(void);
+
+/* ---- context (one execution pool per device) ---------------------------------------- */
+/* Replaces Engine.__init__ (engine.py:161-179). tp_size must be 1 in this build. */
+int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
+                  void* nccl_comm, int64_t kv_pages, int32_t page_size, fp_ctx** out);
+int fp_ctx_destroy(fp_ctx* ctx);
+int fp_ctx_stream(fp_ctx* ctx, void** stream_out); /* cudaStream_t of the prefill stream */
+int fp_ctx_free_pages(fp_ctx* ctx, int64_t* free_pages);
+int fp_ctx_set_window(fp_ctx* ctx, int32_t entries); /* async look-ahead bound */
+int fp_sync(fp_ctx* ctx);
+
+/* ---- weights ------------------------------------------------------------------------ */
+int fp_weights_init_random(fp_ctx* ctx, uint64_t seed, float std);
+int fp_weights_load(fp_ctx* ctx, int32_t tensor, int32_t layer, const void* host_bf16,
+                    int64_t n_elems);
+
+/* ---- task lifecycle ------------------------------------------------------------------ */
+/* Replaces build_timeline + ExecutionTask.__init__ (cost_model.py:191-244, engine.py:84-115):
+ * requests are concatenated, cut into chunks of chunk_tokens (0 = unchunked), and expanded
+ * into n_chunks * num_layers * 5 guarded entries in chunk -> layer -> operator order. */
+int fp_task_create(fp_ctx* ctx, const int32_t* token_ids, const int32_t* seq_lens,
+                   int32_t n_seqs, int32_t chunk_tokens, int32_t granularity, int32_t task_id,
+                   fp_task** out);
+int fp_task_num_entries(const fp_task* task);
+int fp_task_entry_info(const fp_task* task, int32_t entry, int32_t* chunk, int32_t* layer,
+                       int32_t* op, int32_t* new_tokens);
+int fp_task_destroy(fp_ctx* ctx, fp_task* task);
+
+/* Start a new execution segment from `first` (Engine.submit / Engine.resume,
+ * engine.py:207-238): bumps the generation and re-arms the boundary checks of [first, end). */
+int fp_task_begin_segment(fp_ctx* ctx, fp_task* task, int32_t first);
+/* Enqueue entries [first, last) of the current segment on the prefill stream (synchronous
+ * launch, asynchronous execution). Used by the virtual-clock parity driver and the bench. */
+int fp_task_enqueue(fp_ctx* ctx, fp_task* task, int32_t first, int32_t last);
+/* Asynchronous segment: begin_segment(first) + the context's launch worker keeps at most
+ * `window` entries queued ahead of the GPU until the end or a stop. */
+int fp_task_start(fp_ctx* ctx, fp_task* task, int32_t first);
+int fp_task_poll(fp_ctx* ctx, fp_task* task, fp_task_status* out);
+
+/* ---- preemption handshake (Engine.signal_preempt / _finalize_ack, engine.py:240-291) ---- */
+int fp_signal(fp_ctx* ctx);
+int fp_clear(fp_ctx* ctx);
+int fp_poll(fp_ctx* ctx, fp_status* out);
+
+/* ---- parity taps ----------------------------------------------------------------------- */
+int fp_task_logits(fp_ctx* ctx, fp_task* task, float* host_out); /* [n_seqs, vocab] */
+int fp_task_read_kv(fp_ctx* ctx, fp_task* task, int32_t seq, int32_t layer, void* host_k,
+                    void* host_v); /* each [seq_len, n_kv_heads, head_dim] bf16 */
+
+/* ---- per-operator entry points (device pointers; unit tests and microbenchmarks) -------- */
+/* C[M,N] = A[M,K] B[N,K]^T; epi: 0 bf16 store, 1 fp32 store, 2 residual add into C (bf16). */
+int fp_op_gemm(fp_ctx* ctx, int32_t epi, const void* A, const void* B, void* C, int32_t M,
+               int32_t N, int32_t K);
+int fp_op_rmsnorm(fp_ctx* ctx, const void* x, const void* gamma, void* out, int32_t M,
+                  int32_t d, float eps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,125 @@
+"""ctypes binding of the C ABI declared in include/flowprefill.h.
+
+The shared library is built in-tree (``__graft_entry__.build()`` / ``python -m
+paper_2602_16603_b200.build``) into ``paper_2602_16603_b200/_native/libflowprefill.so``.
+There is no fallback: if the library is missing or fails to load, every GPU entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_native", "libflowprefill.so")
+
+FP_OK = 0
+FP_GRAN = {"operator": 0, "layer": 1, "chunk": 2, "none": 3}
+FP_TASK_IDLE, FP_TASK_RUNNING, FP_TASK_STOPPED, FP_TASK_DONE = 0, 1, 2, 3
+
+W_EMBED, W_Q, W_K, W_V, W_O, W_GATE, W_UP, W_DOWN = range(8)
+W_ATTN_NORM, W_FFN_NORM, W_FINAL_NORM, W_LM_HEAD = 8, 9, 10, 11
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned a negative status."""
+
+
+class ModelCfg(C.Structure):
+    _fields_ = [
+        ("num_layers", C.c_int32),
+        ("hidden", C.c_int32),
+        ("n_heads", C.c_int32),
+        ("n_kv_heads", C.c_int32),
+        ("head_dim", C.c_int32),
+        ("ffn", C.c_int32),
+        ("vocab", C.c_int32),
+        ("max_pos", C.c_int32),
+        ("rope_theta", C.c_float),
+        ("rms_eps", C.c_float),
+    ]
+
+
+class Status(C.Structure):
+    _fields_ = [
+        ("ack_seq", C.c_int32),
+        ("ack_task", C.c_int32),
+        ("ack_entry", C.c_int32),
+        ("progress_task", C.c_int32),
+        ("progress_entry", C.c_int32),
+        ("signal", C.c_int32),
+        ("ack_ns", C.c_uint64),
+    ]
+
+
+class TaskStatus(C.Structure):
+    _fields_ = [
+        ("state", C.c_int32),
+        ("cursor", C.c_int32),
+        ("generation", C.c_int32),
+        ("enqueued", C.c_int32),
+    ]
+
+
+# name -> (restype, argtypes)
+_P = C.c_void_p
+_I = C.c_int32
+_SIGS = {
+    "fp_last_error": (C.c_char_p, []),
+    "fp_version": (C.c_int, []),
+    "fp_ctx_create": (C.c_int, [_I, C.POINTER(ModelCfg), _I, _I, _P, C.c_int64, _I, C.POINTER(_P)]),
+    "fp_ctx_destroy": (C.c_int, [_P]),
+    "fp_ctx_stream": (C.c_int, [_P, C.POINTER(_P)]),
+    "fp_ctx_free_pages": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "fp_ctx_set_window": (C.c_int, [_P, _I]),
+    "fp_sync": (C.c_int, [_P]),
+    "fp_weights_init_random": (C.c_int, [_P, C.c_uint64, C.c_float]),
+    "fp_weights_load": (C.c_int, [_P, _I, _I, _P, C.c_int64]),
+    "fp_task_create": (C.c_int, [_P, _P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
+    "fp_task_num_entries": (C.c_int, [_P]),
+    "fp_task_entry_info": (C.c_int, [_P, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+    "fp_task_destroy": (C.c_int, [_P, _P]),
+    "fp_task_begin_segment": (C.c_int, [_P, _P, _I]),
+    "fp_task_enqueue": (C.c_int, [_P, _P, _I, _I]),
+    "fp_task_start": (C.c_int, [_P, _P, _I]),
+    "fp_task_poll": (C.c_int, [_P, _P, C.POINTER(TaskStatus)]),
+    "fp_signal": (C.c_int, [_P]),
+    "fp_clear": (C.c_int, [_P]),
+    "fp_poll": (C.c_int, [_P, C.POINTER(Status)]),
+    "fp_task_logits": (C.c_int, [_P, _P, _P]),
+    "fp_task_read_kv": (C.c_int, [_P, _P, _I, _I, _P, _P]),
+    "fp_op_gemm": (C.c_int, [_P, _I, _P, _P, _P, _I, _I, _I]),
+    "fp_op_rmsnorm": (C.c_int, [_P, _P, _P, _P, _I, _I, C.c_float]),
+}
+
+_lib: Optional[C.CDLL] = None
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load (once) and type the native library. Raises if it is absent: no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeError(
+            f"native library missing: {path}. Build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (nvcc, sm_100a)."
+        )
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != FP_OK:
+        msg = load().fp_last_error().decode(errors="replace")
+        raise NativeError(f"{what or 'native call'} failed ({rc}): {msg}")

@@ -1,0 +1,91 @@
+// Cooperative preemption control: the per-boundary device-side check.
+//
+// The reference models the check as "after the current operator completes, look at the
+// preemption signal; if set, unset it, ACK, and suspend" (simulated in
+// prefillsim/engine.py:240-291). Here every timeline entry's FIRST kernel evaluates the check
+// in its prologue. All CTAs of that kernel agree through one atomicCAS on the entry's decision
+// slot, so a kernel either runs completely or not at all; later kernels of the same entry and
+// every queued entry of a stopped generation become no-ops.
+#pragma once
+#include "common.cuh"
+
+namespace fp {
+
+// Pinned, device-mapped host memory: one per context (one execution pool).
+struct HostCtl {
+  volatile int signal;          // host -> device: 1 = preemption requested
+  volatile int ack_seq;         // device -> host: bumped once per acknowledged stop
+  volatile int ack_task;        // task id that stopped
+  volatile int ack_entry;       // first entry NOT executed (= new cursor)
+  volatile int progress_task;   // task whose entry most recently passed its check
+  volatile int progress_entry;  // that entry's index
+  volatile unsigned long long ack_ns;  // device %globaltimer at the stop decision
+  int pad[24];
+};
+
+// Device memory: one per task. dec[] holds one decision per timeline entry.
+struct TaskCtl {
+  int stopped_gen;  // generation that has been stopped (-1: none)
+  int pad[31];
+  int dec[1];       // [n_entries]: 0 undecided, 1 go, 2 stop
+};
+
+struct Guard {
+  HostCtl* host;  // device alias of the mapped control block (may be null: unguarded)
+  TaskCtl* task;  // null: unguarded launch (per-op unit entry points)
+  int entry;
+  int gen;
+  int task_id;
+  int first;     // 1 for the first kernel of the entry: evaluates the check
+  int eligible;  // the boundary in front of this entry is preemption-eligible
+  int pad;
+};
+
+constexpr int kDecGo = 1;
+constexpr int kDecStop = 2;
+
+// Thread-0-only. Returns true when the kernel must execute.
+DEVI bool guard_pass(const Guard& g) {
+  if (g.task == nullptr) return true;
+  volatile int* sg = &g.task->stopped_gen;
+  if (*sg == g.gen) return false;
+  if (!g.first) return true;
+  volatile int* slot = &g.task->dec[g.entry];
+  const int seen = *slot;  // most CTAs find the decision already made: no atomic needed
+  if (seen) return seen == kDecGo;
+  int want = kDecGo;
+  if (g.eligible && g.host != nullptr && ld_volatile_sys(&g.host->signal)) want = kDecStop;
+  const int old = atomicCAS(&g.task->dec[g.entry], 0, want);
+  const int d = old ? old : want;
+  if (old == 0 && g.host != nullptr) {  // the winning CTA publishes the decision
+    if (d == kDecStop) {
+      *sg = g.gen;
+      __threadfence();
+      g.host->signal = 0;
+      g.host->ack_task = g.task_id;
+      g.host->ack_entry = g.entry;
+      g.host->ack_ns = globaltimer();
+      __threadfence_system();
+      g.host->ack_seq = g.host->ack_seq + 1;
+      __threadfence_system();
+    } else {
+      g.host->progress_task = g.task_id;
+      g.host->progress_entry = g.entry;
+      __threadfence_system();
+    }
+  } else if (old == 0 && d == kDecStop) {
+    *sg = g.gen;
+    __threadfence();
+  }
+  return d == kDecGo;
+}
+
+// Block-wide wrapper; every thread calls it.
+DEVI bool guard_block(const Guard& g) {
+  __shared__ int s_go;
+  if (threadIdx.x == 0) s_go = guard_pass(g) ? 1 : 0;
+  __syncthreads();
+  return s_go != 0;
+}
+
+}  // namespace fp

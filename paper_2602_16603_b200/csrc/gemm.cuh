@@ -1,0 +1,324 @@
+// Persistent, warp-specialised tcgen05 GEMM for the four dense prefill operators.
+//
+//   C[M, N] = A[M, K] * B[N, K]^T      A, B bf16 K-major (row-major, K contiguous)
+//
+// Realises the linear part of the reference's qkv_proj / o_proj / gate_up_proj / down_proj
+// timeline entries (prefillsim/cost_model.py:38-44, 234-242): the GEMM M dimension is the
+// chunk's concatenated token count `new_total` (cost_model.py:225,236).
+//
+// Layout of one CTA (256 threads, 1 CTA / SM, persistent over tiles):
+//   warp 0      TMA producer (A tile 128x64, B tile BNx64 per stage, 128B swizzle)
+//   warp 1      MMA issuer (one thread; tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16)
+//   warp 2      TMEM allocator (2 accumulator stages x BN fp32 columns)
+//   warps 4..7  epilogue: tcgen05.ld (one token row per thread) -> fused epilogue -> HBM
+// The accumulator is double-buffered in TMEM so the epilogue of tile i overlaps the
+// main loop of tile i+1.
+#pragma once
+#include "common.cuh"
+#include "control.cuh"
+
+namespace fp {
+
+enum EpiKind : int {
+  EPI_STORE_BF16 = 0,  // out = bf16(acc)
+  EPI_STORE_F32 = 1,   // out = acc (fp32; lm_head logits)
+  EPI_RESID = 2,       // resid += acc (o_proj, down_proj: residual add)
+  EPI_SWIGLU = 3,      // out = silu(gate) * up; B rows packed [gate(BN/2) | up(BN/2)] per tile
+  EPI_QKV = 4,         // RoPE(q,k); q -> qbuf, k/v -> paged KV cache
+};
+
+struct GemmParams {
+  int M, N, K;
+  int pad0;
+  void* out;
+  long long ldo;
+  __nv_bfloat16* resid;
+  long long ldr;
+  // EPI_QKV
+  const int* pos;       // [M] position of the token inside its own request
+  const int* tok_page;  // [M] physical KV page of the token
+  __nv_bfloat16* qbuf;  // [M, q_cols]
+  long long ldq;
+  __nv_bfloat16* kv_layer;  // this layer's base of the paged KV pool
+  const float2* rope;       // [max_pos][64] (cos, sin)
+  int q_cols, kv_cols, page_size, n_kv_heads;
+  Guard guard;
+};
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBK = 64;
+constexpr int kGemmThreads = 256;
+constexpr int kGemmGroupM = 16;  // m-blocks per raster group (L2 reuse of A and B)
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int A_BYTES = kGemmBM * kGemmBK * 2;
+  static constexpr int B_BYTES = BN * kGemmBK * 2;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+};
+
+DEVI void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = kGemmGroupM * num_n;
+  const int g = t / per_group;
+  const int first_m = g * kGemmGroupM;
+  int gm = num_m - first_m;
+  if (gm > kGemmGroupM) gm = kGemmGroupM;
+  const int local = t - g * per_group;
+  mb = first_m + local % gm;
+  nb = local / gm;
+}
+
+DEVI float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+
+// Store 32 fp32 values as bf16 (64 bytes) to a 16-byte aligned address.
+DEVI void store_row32_bf16(__nv_bfloat16* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 u;
+    u.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+    u.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+    u.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+    u.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+    st_global_v4(dst + 8 * i, u);
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  if (!guard_block(p.guard)) return;
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  const int num_m = (p.M + kGemmBM - 1) / kGemmBM;
+  const int num_n = p.N / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_k = p.K / kGemmBK;
+
+  if (warp == 0) {
+    const uint64_t pol_b = policy_evict_last();
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      for (int kb = 0; kb < num_k; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+          tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kGemmBK, mb * kGemmBM);
+          tma_load_2d_hint(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * kGemmBK, nb * BN, pol_b);
+        }
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = make_idesc_bf16(kGemmBM, BN);
+    int s = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_ph = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tbase + acc * BN;
+      for (int kb = 0; kb < num_k; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint64_t a0 = make_sdesc_sw128(smem_u32(sA + s * Cfg::A_BYTES), 16, 1024);
+          const uint64_t b0 = make_sdesc_sw128(smem_u32(sB + s * Cfg::B_BYTES), 16, 1024);
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k) {
+            // +32 bytes along K inside the 128B swizzle atom (descriptor address is >>4)
+            umma_bf16_ss(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (lane == 0) tc_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quadrant
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_ph = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const uint32_t tacc = tbase + acc * BN + ((uint32_t)(q * 32) << 16);
+      const int m = mb * kGemmBM + row;
+      const bool live = m < p.M;
+      const int n0 = nb * BN;
+
+      if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32 || EPI == EPI_RESID) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tacc + c * 32, r);
+          tmem_ld_wait();
+          if (live) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            if constexpr (EPI == EPI_STORE_F32) {
+              float* dst = reinterpret_cast<float*>(p.out) + (long long)m * p.ldo + n0 + c * 32;
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                st_global_v4(dst + 4 * i, make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                                                     r[4 * i + 3]));
+            } else if constexpr (EPI == EPI_STORE_BF16) {
+              __nv_bfloat16* dst =
+                  reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)m * p.ldo + n0 + c * 32;
+              store_row32_bf16(dst, v);
+            } else {  // EPI_RESID
+              __nv_bfloat16* dst = p.resid + (long long)m * p.ldr + n0 + c * 32;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint4 h = ld_global_v4(dst + 8 * i);
+                const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float2 f = unpack_bf16x2(hw[j]);
+                  v[8 * i + 2 * j] += f.x;
+                  v[8 * i + 2 * j + 1] += f.y;
+                }
+              }
+              store_row32_bf16(dst, v);
+            }
+          }
+        }
+      } else if constexpr (EPI == EPI_SWIGLU) {
+        // Tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows.
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tacc + c * 32, g);
+          tmem_ld32(tacc + BN / 2 + c * 32, u);
+          tmem_ld_wait();
+          if (live) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              v[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)m * p.ldo +
+                                 nb * (BN / 2) + c * 32;
+            store_row32_bf16(dst, v);
+          }
+        }
+      } else {  // EPI_QKV: 128-column heads
+        const int pos = live ? p.pos[m] : 0;
+        const int page = live ? p.tok_page[m] : 0;
+#pragma unroll 1
+        for (int hh = 0; hh < BN / 128; ++hh) {
+          const int col0 = n0 + hh * 128;
+          const bool is_q = col0 < p.q_cols;
+          const bool is_v = col0 >= p.q_cols + p.kv_cols;
+          __nv_bfloat16* dst;
+          if (is_q) {
+            dst = p.qbuf + (long long)m * p.ldq + col0;
+          } else {
+            const int kv = is_v ? 1 : 0;
+            const int h = (col0 - p.q_cols - kv * p.kv_cols) >> 7;
+            dst = p.kv_layer +
+                  ((((long long)page * 2 + kv) * p.n_kv_heads + h) * p.page_size +
+                   (pos % p.page_size)) *
+                      128;
+          }
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            // chunk pair (half, half+2): columns j and j+64 of the head for j in this chunk
+            uint32_t a[32], b[32];
+            tmem_ld32(tacc + hh * 128 + half * 32, a);
+            tmem_ld32(tacc + hh * 128 + half * 32 + 64, b);
+            tmem_ld_wait();
+            if (live) {
+              float x1[32], x2[32];
+              if (!is_v) {
+                const float2* cs = p.rope + (long long)pos * 64 + half * 32;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const float2 t2 = cs[i];
+                  const float u1 = __uint_as_float(a[i]);
+                  const float u2 = __uint_as_float(b[i]);
+                  x1[i] = u1 * t2.x - u2 * t2.y;
+                  x2[i] = u2 * t2.x + u1 * t2.y;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  x1[i] = __uint_as_float(a[i]);
+                  x2[i] = __uint_as_float(b[i]);
+                }
+              }
+              store_row32_bf16(dst + half * 32, x1);
+              store_row32_bf16(dst + half * 32 + 64, x2);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::TMEM_COLS>(tbase);
+  }
+}
+
+}  // namespace fp

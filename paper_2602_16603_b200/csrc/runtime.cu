@@ -1,0 +1,974 @@
+// Native runtime of the preemptible prefill path: context (= execution pool), weights,
+// paged KV pool, task plans (= timelines), guarded entry launches, launch worker, C ABI.
+#include <atomic>
+#include <algorithm>
+#include <cmath>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/flowprefill.h"
+#include "attn_mma.cuh"
+#include "common.cuh"
+#include "control.cuh"
+#include "gemm.cuh"
+#include "norm.cuh"
+
+using namespace fp;
+
+// --------------------------------------------------------------------------- errors
+static thread_local std::string g_err;
+static int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(FP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+#define REQ(cond, msg)                                      \
+  do {                                                      \
+    if (!(cond)) return set_err(FP_ERR_ARG, (msg));         \
+  } while (0)
+
+// --------------------------------------------------------------------------- TMA maps
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+// 2D bf16 row-major [rows, cols], box = [box_rows, 64 cols], 128B swizzle.
+static int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+                    uint32_t box_rows) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return set_err(FP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(FP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return FP_OK;
+}
+
+// --------------------------------------------------------------------------- random init
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void init_normal_kernel(__nv_bfloat16* w, long long n, uint64_t seed, float mean,
+                                   float stdv) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t r = splitmix64(seed ^ (uint64_t)(i * 0x2545F4914F6CDD1Dull));
+    const float u1 = ((r >> 40) + 1) * (1.0f / 16777217.0f);
+    const float u2 = ((r & 0xFFFFFF)) * (1.0f / 16777216.0f);
+    const float z = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+    w[i] = __float2bfloat16(mean + stdv * z);
+  }
+}
+
+// --------------------------------------------------------------------------- structures
+struct Layer {
+  __nv_bfloat16 *wqkv, *wo, *wgu, *wd, *attn_g, *ffn_g;
+  CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
+};
+
+struct ChunkPlan {
+  int M;          // new tokens in the chunk (cost_model.py:225 new_total)
+  int tok0;       // first token of the chunk in the task's concatenated stream
+  int item0, n_items;
+  int last0, n_last, seq0;  // requests completing in this chunk: rows at last_rows[last0..]
+};
+
+struct Task {
+  int id = 0;
+  int n_seqs = 0, total = 0, L = 0, n_entries = 0, max_m = 0, granularity = 0;
+  std::vector<int> lens;
+  std::vector<ChunkPlan> chunks;
+  std::vector<int> pages;  // KV pages owned
+  int bt_stride = 0;
+  // device
+  char* meta = nullptr;  // one allocation: ids | pos | tok_page | items | bt | last_rows
+  int *d_ids, *d_pos, *d_tpage, *d_bt, *d_last;
+  AttnItem* d_items;
+  __nv_bfloat16 *h, *xn, *q, *ao, *act, *xf;
+  float* logits;
+  TaskCtl* ctl;
+  CUtensorMap tm_xn, tm_ao, tm_act, tm_xf;
+  cudaEvent_t ready, done;
+  // host execution state
+  int gen = 0, seg_first = 0, enq = 0, seg_ack0 = 0, done_recorded = 0;
+  std::atomic<int> worker_active{0};
+};
+
+struct fp_ctx {
+  int device = 0, num_sms = 148;
+  fp_model_cfg cfg{};
+  int qdim = 0, kvdim = 0, qkv_n = 0;
+  cudaStream_t stream = nullptr, upload = nullptr;
+  std::vector<Layer> layers;
+  __nv_bfloat16 *embed = nullptr, *final_g = nullptr, *lm_head = nullptr;
+  CUtensorMap tm_lm;
+  float2* rope = nullptr;
+  __nv_bfloat16* kv = nullptr;
+  long long page_elems = 0;  // elements of one page in one layer (2*Hkv*PS*hd)
+  int page_size = 128;
+  long long kv_pages = 0;
+  std::vector<int> free_pages;
+  std::mutex page_mu;
+  HostCtl* hctl = nullptr;   // host view
+  HostCtl* dctl = nullptr;   // device alias
+  std::mutex launch_mu;
+  // worker
+  std::thread worker;
+  std::mutex wmu;
+  std::condition_variable wcv;
+  Task* wtask = nullptr;
+  bool wquit = false;
+  int window = 8;
+};
+
+// --------------------------------------------------------------------------- launches
+template <int EPI>
+static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
+                        const GemmParams& p, cudaStream_t st) {
+  constexpr int BN = 256;
+  auto kern = gemm_bf16_tn_kernel<BN, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GemmCfg<BN>::SMEM_BYTES);
+    attr = true;
+  }
+  const int tiles = ((p.M + kGemmBM - 1) / kGemmBM) * (p.N / BN);
+  const int grid = std::max(1, std::min(tiles, c->num_sms));
+  kern<<<grid, kGemmThreads, GemmCfg<BN>::SMEM_BYTES, st>>>(a, b, p);
+}
+
+static int launch_rms(const RmsParams& p, cudaStream_t st) {
+  const int grid = (p.M + kRmsRowsPerBlock - 1) / kRmsRowsPerBlock;
+  if (grid == 0) return FP_OK;
+  switch (p.d / 256) {
+    case 2: rmsnorm_kernel<2><<<grid, 256, 0, st>>>(p); break;
+    case 4: rmsnorm_kernel<4><<<grid, 256, 0, st>>>(p); break;
+    case 8: rmsnorm_kernel<8><<<grid, 256, 0, st>>>(p); break;
+    case 16: rmsnorm_kernel<16><<<grid, 256, 0, st>>>(p); break;
+    case 20: rmsnorm_kernel<20><<<grid, 256, 0, st>>>(p); break;
+    default: return set_err(FP_ERR_UNSUPPORTED, "rmsnorm: unsupported hidden size");
+  }
+  return FP_OK;
+}
+
+static void launch_attn(const AttnParams& p, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_prefill_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kAttnMmaSmem);
+    attr = true;
+  }
+  dim3 grid(p.n_items, p.n_heads);
+  attn_prefill_mma_kernel<<<grid, mmaattn::THREADS, kAttnMmaSmem, st>>>(p);
+}
+
+static bool boundary_eligible(const fp_ctx* c, int gran, int i, int n_entries) {
+  // eligibility of the boundary AFTER entry i (engine.py:127-134 with layer_last/chunk_last)
+  const int L = c->cfg.num_layers;
+  const int op = i % 5;
+  const int layer = (i / 5) % L;
+  if (gran == FP_GRAN_OPERATOR) return true;
+  if (gran == FP_GRAN_LAYER) return op == 4 || i == n_entries - 1;
+  if (gran == FP_GRAN_CHUNK) return (op == 4 && layer == L - 1) || i == n_entries - 1;
+  return false;
+}
+
+// Enqueue the kernels of one timeline entry. Caller holds launch_mu.
+static int launch_entry(fp_ctx* c, Task* t, int e) {
+  const fp_model_cfg& m = c->cfg;
+  const int L = m.num_layers;
+  const int ci = e / (5 * L);
+  const int layer = (e / 5) % L;
+  const int op = e % 5;
+  const ChunkPlan& ch = t->chunks[ci];
+  const int M = ch.M;
+  cudaStream_t st = c->stream;
+  Layer& ly = c->layers[layer];
+
+  Guard g{};
+  g.host = c->dctl;
+  g.task = t->ctl;
+  g.entry = e;
+  g.gen = t->gen;
+  g.task_id = t->id;
+  g.first = 1;
+  g.eligible = (e != t->seg_first) && boundary_eligible(c, t->granularity, e - 1, t->n_entries);
+  Guard g2 = g;
+  g2.first = 0;
+
+  const int* ids = t->d_ids + ch.tok0;
+  const int* pos = t->d_pos + ch.tok0;
+  const int* tpage = t->d_tpage + ch.tok0;
+  __nv_bfloat16* kv_layer = c->kv + (long long)layer * c->kv_pages * c->page_elems;
+
+  if (op == FP_OP_QKV_PROJ || op == FP_OP_GATE_UP_PROJ) {
+    RmsParams r{};
+    r.M = M;
+    r.d = m.hidden;
+    r.src = t->h;
+    r.ld_src = m.hidden;
+    if (op == FP_OP_QKV_PROJ && layer == 0) {  // chunk start: embedding gather into h
+      r.src = c->embed;
+      r.ids = ids;
+      r.h_out = t->h;
+      r.ld_h = m.hidden;
+    }
+    r.gamma = op == FP_OP_QKV_PROJ ? ly.attn_g : ly.ffn_g;
+    r.out = t->xn;
+    r.ld_out = m.hidden;
+    r.eps = m.rms_eps;
+    r.guard = g;
+    int rc = launch_rms(r, st);
+    if (rc) return rc;
+    GemmParams p{};
+    p.M = M;
+    p.K = m.hidden;
+    p.guard = g2;
+    if (op == FP_OP_QKV_PROJ) {
+      p.N = c->qkv_n;
+      p.pos = pos;
+      p.tok_page = tpage;
+      p.qbuf = t->q;
+      p.ldq = c->qdim;
+      p.kv_layer = kv_layer;
+      p.rope = c->rope;
+      p.q_cols = c->qdim;
+      p.kv_cols = c->kvdim;
+      p.page_size = c->page_size;
+      p.n_kv_heads = m.n_kv_heads;
+      launch_gemm<EPI_QKV>(c, t->tm_xn, ly.tm_qkv, p, st);
+    } else {
+      p.N = 2 * m.ffn;
+      p.out = t->act;
+      p.ldo = m.ffn;
+      launch_gemm<EPI_SWIGLU>(c, t->tm_xn, ly.tm_gu, p, st);
+    }
+  } else if (op == FP_OP_ATTN) {
+    AttnParams a{};
+    a.items = t->d_items + ch.item0;
+    a.n_items = ch.n_items;
+    a.n_heads = m.n_heads;
+    a.q = t->q;
+    a.ldq = c->qdim;
+    a.out = t->ao;
+    a.ldo = c->qdim;
+    a.kv_layer = kv_layer;
+    a.block_table = t->d_bt;
+    a.bt_stride = t->bt_stride;
+    a.n_kv_heads = m.n_kv_heads;
+    a.page_size = c->page_size;
+    a.scale_log2 = 1.4426950408889634f / sqrtf((float)m.head_dim);
+    a.guard = g;
+    if (a.n_items > 0) launch_attn(a, st);
+  } else {  // O_PROJ / DOWN_PROJ: residual add
+    GemmParams p{};
+    p.M = M;
+    p.N = m.hidden;
+    p.resid = t->h;
+    p.ldr = m.hidden;
+    p.guard = g;
+    if (op == FP_OP_O_PROJ) {
+      p.K = c->qdim;
+      launch_gemm<EPI_RESID>(c, t->tm_ao, ly.tm_o, p, st);
+    } else {
+      p.K = m.ffn;
+      launch_gemm<EPI_RESID>(c, t->tm_act, ly.tm_d, p, st);
+      if (layer == L - 1 && ch.n_last > 0) {  // completion: final norm + lm_head of last tokens
+        RmsParams r{};
+        r.M = ch.n_last;
+        r.d = m.hidden;
+        r.src = t->h;
+        r.ld_src = m.hidden;
+        r.rows = t->d_last + ch.last0;
+        r.gamma = c->final_g;
+        r.out = t->xf;
+        r.ld_out = m.hidden;
+        r.eps = m.rms_eps;
+        r.guard = g2;
+        int rc = launch_rms(r, st);
+        if (rc) return rc;
+        GemmParams q{};
+        q.M = ch.n_last;
+        q.N = m.vocab;
+        q.K = m.hidden;
+        q.out = t->logits + (long long)ch.seq0 * m.vocab;
+        q.ldo = m.vocab;
+        q.guard = g2;
+        launch_gemm<EPI_STORE_F32>(c, t->tm_xf, c->tm_lm, q, st);
+      }
+    }
+  }
+  return FP_OK;
+}
+
+// --------------------------------------------------------------------------- worker
+static void worker_main(fp_ctx* c) {
+  cudaSetDevice(c->device);
+  for (;;) {
+    Task* t = nullptr;
+    {
+      std::unique_lock<std::mutex> lk(c->wmu);
+      c->wcv.wait(lk, [&] { return c->wquit || c->wtask != nullptr; });
+      if (c->wquit) return;
+      t = c->wtask;
+    }
+    while (t->enq < t->n_entries) {
+      if (c->hctl->ack_seq != t->seg_ack0) break;  // stopped: leave the rest unlaunched
+      int prog = t->seg_first - 1;
+      if (c->hctl->progress_task == t->id) prog = std::max(prog, (int)c->hctl->progress_entry);
+      if (t->enq - prog <= c->window) {
+        std::lock_guard<std::mutex> lk(c->launch_mu);
+        launch_entry(c, t, t->enq);
+        t->enq++;
+      } else {
+        std::this_thread::yield();
+      }
+    }
+    {
+      std::lock_guard<std::mutex> lk(c->launch_mu);
+      cudaEventRecord(t->done, c->stream);
+      t->done_recorded = 1;
+    }
+    {
+      std::lock_guard<std::mutex> lk(c->wmu);
+      c->wtask = nullptr;
+    }
+    t->worker_active.store(0);
+  }
+}
+
+// --------------------------------------------------------------------------- C ABI
+extern "C" {
+
+const char* fp_last_error(void) { return g_err.c_str(); }
+int fp_version(void) { return 1; }
+
+int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
+                  void* nccl_comm, int64_t kv_pages, int32_t page_size, fp_ctx** out) {
+  (void)tp_rank;
+  (void)nccl_comm;
+  REQ(cfg && out, "null argument");
+  REQ(tp_size == 1, "tensor parallelism is not built into this library version");
+  REQ(cfg->head_dim == 128, "head_dim must be 128");
+  REQ(cfg->hidden % 256 == 0 && cfg->ffn % 128 == 0, "hidden%256 and ffn%128 required");
+  REQ(cfg->n_heads % cfg->n_kv_heads == 0, "n_heads must be a multiple of n_kv_heads");
+  REQ(((cfg->n_heads + 2 * cfg->n_kv_heads) * 128) % 256 == 0, "qkv width must be %256");
+  REQ(cfg->vocab % 256 == 0, "vocab must be a multiple of 256");
+  REQ(page_size > 0 && page_size % 64 == 0, "page_size must be a multiple of 64");
+  REQ(kv_pages > 0, "kv_pages must be > 0");
+  CK(cudaSetDevice(device));
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) return set_err(FP_ERR_UNSUPPORTED, "requires an sm_100 (B200) device");
+  fp_ctx* c = new fp_ctx();
+  c->device = device;
+  c->cfg = *cfg;
+  c->qdim = cfg->n_heads * 128;
+  c->kvdim = cfg->n_kv_heads * 128;
+  c->qkv_n = c->qdim + 2 * c->kvdim;
+  c->page_size = page_size;
+  c->kv_pages = kv_pages;
+  c->page_elems = 2LL * cfg->n_kv_heads * page_size * 128;
+  CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
+  // let the async mempool keep freed task workspaces
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thresh = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+
+  const int L = cfg->num_layers, d = cfg->hidden;
+  c->layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    Layer& ly = c->layers[l];
+    CK(cudaMalloc(&ly.wqkv, (size_t)c->qkv_n * d * 2));
+    CK(cudaMalloc(&ly.wo, (size_t)d * c->qdim * 2));
+    CK(cudaMalloc(&ly.wgu, (size_t)2 * cfg->ffn * d * 2));
+    CK(cudaMalloc(&ly.wd, (size_t)d * cfg->ffn * 2));
+    CK(cudaMalloc(&ly.attn_g, (size_t)d * 2));
+    CK(cudaMalloc(&ly.ffn_g, (size_t)d * 2));
+    int rc;
+    if ((rc = make_map(&ly.tm_qkv, ly.wqkv, c->qkv_n, d, 256))) return rc;
+    if ((rc = make_map(&ly.tm_o, ly.wo, d, c->qdim, 256))) return rc;
+    if ((rc = make_map(&ly.tm_gu, ly.wgu, 2 * cfg->ffn, d, 256))) return rc;
+    if ((rc = make_map(&ly.tm_d, ly.wd, d, cfg->ffn, 256))) return rc;
+  }
+  CK(cudaMalloc(&c->embed, (size_t)cfg->vocab * d * 2));
+  CK(cudaMalloc(&c->lm_head, (size_t)cfg->vocab * d * 2));
+  CK(cudaMalloc(&c->final_g, (size_t)d * 2));
+  {
+    int rc = make_map(&c->tm_lm, c->lm_head, cfg->vocab, d, 256);
+    if (rc) return rc;
+  }
+  // RoPE table (rotate-half convention), fp64 on the host
+  {
+    std::vector<float2> tab((size_t)cfg->max_pos * 64);
+    for (int p = 0; p < cfg->max_pos; ++p)
+      for (int j = 0; j < 64; ++j) {
+        const double inv = 1.0 / std::pow((double)cfg->rope_theta, (2.0 * j) / 128.0);
+        const double a = (double)p * inv;
+        tab[(size_t)p * 64 + j] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+    CK(cudaMalloc(&c->rope, tab.size() * sizeof(float2)));
+    CK(cudaMemcpy(c->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMalloc(&c->kv, (size_t)L * kv_pages * c->page_elems * 2));
+  c->free_pages.resize(kv_pages);
+  for (long long i = 0; i < kv_pages; ++i) c->free_pages[i] = (int)(kv_pages - 1 - i);
+  CK(cudaHostAlloc(&c->hctl, sizeof(HostCtl), cudaHostAllocMapped));
+  memset((void*)c->hctl, 0, sizeof(HostCtl));
+  c->hctl->progress_task = -1;
+  CK(cudaHostGetDevicePointer((void**)&c->dctl, (void*)c->hctl, 0));
+  c->worker = std::thread(worker_main, c);
+  *out = c;
+  return FP_OK;
+}
+
+int fp_ctx_destroy(fp_ctx* c) {
+  if (!c) return FP_OK;
+  {
+    std::lock_guard<std::mutex> lk(c->wmu);
+    c->wquit = true;
+  }
+  c->wcv.notify_all();
+  if (c->worker.joinable()) c->worker.join();
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& ly : c->layers) {
+    cudaFree(ly.wqkv);
+    cudaFree(ly.wo);
+    cudaFree(ly.wgu);
+    cudaFree(ly.wd);
+    cudaFree(ly.attn_g);
+    cudaFree(ly.ffn_g);
+  }
+  cudaFree(c->embed);
+  cudaFree(c->lm_head);
+  cudaFree(c->final_g);
+  cudaFree(c->rope);
+  cudaFree(c->kv);
+  cudaFreeHost((void*)c->hctl);
+  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->upload);
+  delete c;
+  return FP_OK;
+}
+
+int fp_ctx_stream(fp_ctx* c, void** s) {
+  REQ(c && s, "null argument");
+  *s = (void*)c->stream;
+  return FP_OK;
+}
+int fp_ctx_free_pages(fp_ctx* c, int64_t* n) {
+  REQ(c && n, "null argument");
+  std::lock_guard<std::mutex> lk(c->page_mu);
+  *n = (int64_t)c->free_pages.size();
+  return FP_OK;
+}
+int fp_ctx_set_window(fp_ctx* c, int32_t w) {
+  REQ(c && w >= 1, "window must be >= 1");
+  c->window = w;
+  return FP_OK;
+}
+int fp_sync(fp_ctx* c) {
+  REQ(c, "null ctx");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  return FP_OK;
+}
+
+static __nv_bfloat16* weight_ptr(fp_ctx* c, int tensor, int layer, long long* n_out,
+                                 long long* off) {
+  const fp_model_cfg& m = c->cfg;
+  const long long d = m.hidden;
+  *off = 0;
+  Layer* ly = (layer >= 0 && layer < m.num_layers) ? &c->layers[layer] : nullptr;
+  switch (tensor) {
+    case FP_W_EMBED: *n_out = (long long)m.vocab * d; return c->embed;
+    case FP_W_LM_HEAD: *n_out = (long long)m.vocab * d; return c->lm_head;
+    case FP_W_FINAL_NORM: *n_out = d; return c->final_g;
+    default: break;
+  }
+  if (!ly) return nullptr;
+  switch (tensor) {
+    case FP_W_Q: *n_out = c->qdim * d; return ly->wqkv;
+    case FP_W_K: *n_out = c->kvdim * d; *off = c->qdim * d; return ly->wqkv;
+    case FP_W_V: *n_out = c->kvdim * d; *off = (c->qdim + c->kvdim) * d; return ly->wqkv;
+    case FP_W_O: *n_out = d * c->qdim; return ly->wo;
+    case FP_W_GATE: *n_out = (long long)m.ffn * d; return ly->wgu;
+    case FP_W_UP: *n_out = (long long)m.ffn * d; return ly->wgu;
+    case FP_W_DOWN: *n_out = d * m.ffn; return ly->wd;
+    case FP_W_ATTN_NORM: *n_out = d; return ly->attn_g;
+    case FP_W_FFN_NORM: *n_out = d; return ly->ffn_g;
+  }
+  return nullptr;
+}
+
+int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, int64_t n) {
+  REQ(c && host, "null argument");
+  CK(cudaSetDevice(c->device));
+  long long need = 0, off = 0;
+  __nv_bfloat16* dst = weight_ptr(c, tensor, layer, &need, &off);
+  REQ(dst != nullptr, "unknown tensor/layer");
+  REQ(n == need, "weight size mismatch");
+  if (tensor == FP_W_GATE || tensor == FP_W_UP) {
+    // pack gate/up interleaved in blocks of 128 rows: [g(128) | u(128)] per 256-row block,
+    // so one 256-wide GEMM tile holds matching gate and up columns (SwiGLU epilogue).
+    const int d = c->cfg.hidden;
+    const int blocks = c->cfg.ffn / 128;
+    const char* src = static_cast<const char*>(host);
+    const int half = tensor == FP_W_UP ? 1 : 0;
+    for (int b = 0; b < blocks; ++b)
+      CK(cudaMemcpy(dst + ((size_t)b * 256 + half * 128) * d, src + (size_t)b * 128 * d * 2,
+                    (size_t)128 * d * 2, cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemcpy(dst + off, host, (size_t)n * 2, cudaMemcpyHostToDevice));
+  }
+  return FP_OK;
+}
+
+int fp_weights_init_random(fp_ctx* c, uint64_t seed, float stdv) {
+  REQ(c, "null ctx");
+  CK(cudaSetDevice(c->device));
+  const fp_model_cfg& m = c->cfg;
+  const long long d = m.hidden;
+  uint64_t s = seed * 1000003ull;
+  auto fill = [&](__nv_bfloat16* p, long long n, float mean, float sd) {
+    init_normal_kernel<<<1184, 256, 0, c->stream>>>(p, n, s++, mean, sd);
+  };
+  fill(c->embed, (long long)m.vocab * d, 0.f, stdv);
+  fill(c->lm_head, (long long)m.vocab * d, 0.f, stdv);
+  fill(c->final_g, d, 1.f, 0.1f);
+  for (auto& ly : c->layers) {
+    fill(ly.wqkv, (long long)c->qkv_n * d, 0.f, stdv);
+    fill(ly.wo, d * c->qdim, 0.f, stdv);
+    fill(ly.wgu, 2LL * m.ffn * d, 0.f, stdv);
+    fill(ly.wd, d * m.ffn, 0.f, stdv);
+    fill(ly.attn_g, d, 1.f, 0.1f);
+    fill(ly.ffn_g, d, 1.f, 0.1f);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return FP_OK;
+}
+
+int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n_seqs,
+                   int32_t chunk_tokens, int32_t granularity, int32_t task_id, fp_task** out) {
+  REQ(c && ids && lens && out, "null argument");
+  REQ(n_seqs >= 1, "per_request_tokens must be non-empty");  // cost_model.py:205-206
+  REQ(chunk_tokens >= 0, "chunk_tokens must be >= 0");
+  REQ(granularity >= 0 && granularity <= 3, "bad granularity");
+  const fp_model_cfg& m = c->cfg;
+  CK(cudaSetDevice(c->device));
+  Task* t = new Task();
+  t->id = task_id;
+  t->n_seqs = n_seqs;
+  t->L = m.num_layers;
+  t->granularity = granularity;
+  t->lens.assign(lens, lens + n_seqs);
+  long long total = 0;
+  for (int i = 0; i < n_seqs; ++i) {
+    if (lens[i] < 1) {
+      delete t;
+      return set_err(FP_ERR_ARG, "all token counts must be >= 1");  // cost_model.py:207-208
+    }
+    if (lens[i] > m.max_pos) {
+      delete t;
+      return set_err(FP_ERR_ARG, "request longer than max_pos");
+    }
+    total += lens[i];
+  }
+  t->total = (int)total;
+  for (long long i = 0; i < total; ++i)
+    if (ids[i] < 0 || ids[i] >= m.vocab) {
+      delete t;
+      return set_err(FP_ERR_ARG, "token id out of range");
+    }
+  // pages
+  const int PS = c->page_size;
+  std::vector<int> npages(n_seqs);
+  int need = 0, maxp = 0;
+  for (int i = 0; i < n_seqs; ++i) {
+    npages[i] = (lens[i] + PS - 1) / PS;
+    need += npages[i];
+    maxp = std::max(maxp, npages[i]);
+  }
+  {
+    std::lock_guard<std::mutex> lk(c->page_mu);
+    if ((int)c->free_pages.size() < need) {
+      delete t;
+      return set_err(FP_ERR_NOMEM, "KV page pool exhausted");
+    }
+    for (int i = 0; i < need; ++i) {
+      t->pages.push_back(c->free_pages.back());
+      c->free_pages.pop_back();
+    }
+  }
+  t->bt_stride = maxp;
+  std::vector<int> bt((size_t)n_seqs * maxp, 0);
+  {
+    int k = 0;
+    for (int i = 0; i < n_seqs; ++i)
+      for (int j = 0; j < npages[i]; ++j) bt[(size_t)i * maxp + j] = t->pages[k++];
+  }
+  // chunk plan: cost_model.py:212-233 (requests concatenated, chunks over the stream)
+  std::vector<long long> starts(n_seqs + 1, 0);
+  for (int i = 0; i < n_seqs; ++i) starts[i + 1] = starts[i] + lens[i];
+  std::vector<std::pair<long long, long long>> bounds;
+  if (chunk_tokens == 0 || chunk_tokens >= total) bounds.push_back({0, total});
+  else
+    for (long long lo = 0; lo < total; lo += chunk_tokens)
+      bounds.push_back({lo, std::min(lo + chunk_tokens, total)});
+  std::vector<int> pos(total), tpage(total), last_rows;
+  std::vector<AttnItem> items;
+  for (int i = 0; i < n_seqs; ++i)
+    for (int p = 0; p < lens[i]; ++p) {
+      pos[starts[i] + p] = p;
+      tpage[starts[i] + p] = bt[(size_t)i * maxp + p / PS];
+    }
+  for (auto& b : bounds) {
+    ChunkPlan ch{};
+    const long long s = b.first, e = b.second;
+    ch.M = (int)(e - s);
+    ch.tok0 = (int)s;
+    ch.item0 = (int)items.size();
+    ch.last0 = (int)last_rows.size();
+    ch.seq0 = -1;
+    std::vector<AttnItem> its;
+    for (int r = 0; r < n_seqs; ++r) {
+      const long long r0 = starts[r], r1 = starts[r + 1];
+      const long long share = std::min(e, r1) - std::max(s, r0);
+      if (share <= 0) continue;
+      const long long prefix = std::min(std::max(s - r0, 0LL), (long long)lens[r]);
+      const int row0 = (int)(std::max(s, r0) - s);
+      for (long long k = 0; k < share; k += 64) {
+        AttnItem it;
+        it.q_row0 = row0 + (int)k;
+        it.n_rows = (int)std::min(64LL, share - k);
+        it.q_pos0 = (int)(prefix + k);
+        it.req = r;
+        its.push_back(it);
+      }
+      if (r1 - 1 >= s && r1 - 1 < e) {  // request completes in this chunk
+        if (ch.seq0 < 0) ch.seq0 = r;
+        last_rows.push_back((int)(r1 - 1 - s));
+      }
+    }
+    std::stable_sort(its.begin(), its.end(), [](const AttnItem& a, const AttnItem& b) {
+      return a.q_pos0 + a.n_rows > b.q_pos0 + b.n_rows;  // longest KV range first
+    });
+    items.insert(items.end(), its.begin(), its.end());
+    ch.n_items = (int)items.size() - ch.item0;
+    ch.n_last = (int)last_rows.size() - ch.last0;
+    if (ch.seq0 < 0) ch.seq0 = 0;
+    t->max_m = std::max(t->max_m, ch.M);
+    t->chunks.push_back(ch);
+  }
+  t->n_entries = (int)t->chunks.size() * m.num_layers * 5;
+  // device metadata, one allocation
+  const size_t n_ids = total, n_items = items.size(), n_bt = bt.size(), n_last = last_rows.size();
+  const size_t bytes = (3 * n_ids + n_bt + n_last) * 4 + n_items * sizeof(AttnItem) + 64;
+  std::vector<char> host(bytes, 0);
+  size_t o = 0;
+  auto put = [&](const void* src, size_t nb) {
+    size_t at = o;
+    if (nb) memcpy(host.data() + o, src, nb);
+    o += (nb + 15) & ~size_t(15);
+    return at;
+  };
+  host.resize(bytes + 6 * 16);
+  const size_t o_ids = put(ids, n_ids * 4), o_pos = put(pos.data(), n_ids * 4),
+               o_tp = put(tpage.data(), n_ids * 4), o_it = put(items.data(), n_items * sizeof(AttnItem)),
+               o_bt = put(bt.data(), n_bt * 4), o_last = put(last_rows.data(), n_last * 4);
+  CK(cudaMalloc(&t->meta, o + 16));
+  CK(cudaMemcpy(t->meta, host.data(), o, cudaMemcpyHostToDevice));
+  t->d_ids = reinterpret_cast<int*>(t->meta + o_ids);
+  t->d_pos = reinterpret_cast<int*>(t->meta + o_pos);
+  t->d_tpage = reinterpret_cast<int*>(t->meta + o_tp);
+  t->d_items = reinterpret_cast<AttnItem*>(t->meta + o_it);
+  t->d_bt = reinterpret_cast<int*>(t->meta + o_bt);
+  t->d_last = reinterpret_cast<int*>(t->meta + o_last);
+  // workspaces (resume state lives here: h + the live intermediate)
+  const long long M = t->max_m, d = m.hidden;
+  CK(cudaMalloc(&t->h, M * d * 2));
+  CK(cudaMalloc(&t->xn, M * d * 2));
+  CK(cudaMalloc(&t->q, M * c->qdim * 2));
+  CK(cudaMalloc(&t->ao, M * c->qdim * 2));
+  CK(cudaMalloc(&t->act, M * (long long)m.ffn * 2));
+  CK(cudaMalloc(&t->xf, (long long)n_seqs * d * 2));
+  CK(cudaMalloc(&t->logits, (long long)n_seqs * m.vocab * 4));
+  CK(cudaMemset(t->logits, 0, (long long)n_seqs * m.vocab * 4));
+  const size_t ctl_bytes = sizeof(TaskCtl) + (size_t)t->n_entries * 4;
+  CK(cudaMalloc(&t->ctl, ctl_bytes));
+  CK(cudaMemset(t->ctl, 0, ctl_bytes));
+  CK(cudaMemset(&t->ctl->stopped_gen, 0xFF, 4));  // -1
+  int rc;
+  if ((rc = make_map(&t->tm_xn, t->xn, M, d, 128))) return rc;
+  if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
+  if ((rc = make_map(&t->tm_act, t->act, M, m.ffn, 128))) return rc;
+  if ((rc = make_map(&t->tm_xf, t->xf, n_seqs, d, 128))) return rc;
+  CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+  *out = reinterpret_cast<fp_task*>(t);
+  return FP_OK;
+}
+
+int fp_task_num_entries(const fp_task* task) {
+  return reinterpret_cast<const Task*>(task)->n_entries;
+}
+
+int fp_task_entry_info(const fp_task* task, int32_t e, int32_t* chunk, int32_t* layer,
+                       int32_t* op, int32_t* new_tokens) {
+  const Task* t = reinterpret_cast<const Task*>(task);
+  REQ(t && e >= 0 && e < t->n_entries, "entry out of range");
+  const int ci = e / (5 * t->L);
+  if (chunk) *chunk = ci;
+  if (layer) *layer = (e / 5) % t->L;
+  if (op) *op = e % 5;
+  if (new_tokens) *new_tokens = t->chunks[ci].M;
+  return FP_OK;
+}
+
+int fp_task_destroy(fp_ctx* c, fp_task* task) {
+  Task* t = reinterpret_cast<Task*>(task);
+  if (!t) return FP_OK;
+  REQ(c, "null ctx");
+  CK(cudaSetDevice(c->device));
+  while (t->worker_active.load()) std::this_thread::yield();
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(t->meta);
+  cudaFree(t->h);
+  cudaFree(t->xn);
+  cudaFree(t->q);
+  cudaFree(t->ao);
+  cudaFree(t->act);
+  cudaFree(t->xf);
+  cudaFree(t->logits);
+  cudaFree(t->ctl);
+  cudaEventDestroy(t->done);
+  {
+    std::lock_guard<std::mutex> lk(c->page_mu);
+    for (int p : t->pages) c->free_pages.push_back(p);
+  }
+  delete t;
+  return FP_OK;
+}
+
+int fp_task_begin_segment(fp_ctx* c, fp_task* task, int32_t first) {
+  Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && t, "null argument");
+  REQ(first >= 0 && first < t->n_entries, "segment start out of range");
+  REQ(!t->worker_active.load(), "task is already running");
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  t->gen += 1;
+  t->seg_first = first;
+  t->enq = first;
+  t->done_recorded = 0;
+  t->seg_ack0 = c->hctl->ack_seq;
+  CK(cudaMemsetAsync(&t->ctl->dec[first], 0, (size_t)(t->n_entries - first) * 4, c->stream));
+  return FP_OK;
+}
+
+int fp_task_enqueue(fp_ctx* c, fp_task* task, int32_t first, int32_t last) {
+  Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && t, "null argument");
+  REQ(first >= t->seg_first && first <= last && last <= t->n_entries, "bad entry range");
+  CK(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  for (int e = first; e < last; ++e) {
+    int rc = launch_entry(c, t, e);
+    if (rc) return rc;
+  }
+  t->enq = std::max(t->enq, (int)last);
+  if (last == t->n_entries) {
+    CK(cudaEventRecord(t->done, c->stream));
+    t->done_recorded = 1;
+  }
+  CK(cudaGetLastError());
+  return FP_OK;
+}
+
+int fp_task_start(fp_ctx* c, fp_task* task, int32_t first) {
+  Task* t = reinterpret_cast<Task*>(task);
+  int rc = fp_task_begin_segment(c, task, first);
+  if (rc) return rc;
+  {
+    std::lock_guard<std::mutex> lk(c->wmu);
+    if (c->wtask != nullptr) return set_err(FP_ERR_STATE, "pool occupied");
+    t->worker_active.store(1);
+    c->wtask = t;
+  }
+  c->wcv.notify_all();
+  return FP_OK;
+}
+
+int fp_task_poll(fp_ctx* c, fp_task* task, fp_task_status* st) {
+  Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && t && st, "null argument");
+  st->generation = t->gen;
+  st->enqueued = t->enq;
+  const int ack_seq = c->hctl->ack_seq;
+  const bool stopped = ack_seq != t->seg_ack0 && c->hctl->ack_task == t->id;
+  if (stopped) {
+    st->state = FP_TASK_STOPPED;
+    st->cursor = c->hctl->ack_entry;
+    return FP_OK;
+  }
+  if (t->done_recorded && !t->worker_active.load()) {
+    cudaError_t q = cudaEventQuery(t->done);
+    if (q == cudaSuccess) {
+      // re-check the ACK after the event: a stop in the last launched entries wins
+      if (c->hctl->ack_seq != t->seg_ack0 && c->hctl->ack_task == t->id) {
+        st->state = FP_TASK_STOPPED;
+        st->cursor = c->hctl->ack_entry;
+      } else {
+        st->state = FP_TASK_DONE;
+        st->cursor = t->n_entries;
+      }
+      return FP_OK;
+    }
+    if (q != cudaErrorNotReady) CK(q);
+  }
+  st->state = FP_TASK_RUNNING;
+  st->cursor = (c->hctl->progress_task == t->id) ? (int)c->hctl->progress_entry : t->seg_first;
+  return FP_OK;
+}
+
+int fp_signal(fp_ctx* c) {
+  REQ(c, "null ctx");
+  c->hctl->signal = 1;
+  return FP_OK;
+}
+int fp_clear(fp_ctx* c) {
+  REQ(c, "null ctx");
+  c->hctl->signal = 0;
+  return FP_OK;
+}
+int fp_poll(fp_ctx* c, fp_status* s) {
+  REQ(c && s, "null argument");
+  s->ack_seq = c->hctl->ack_seq;
+  s->ack_task = c->hctl->ack_task;
+  s->ack_entry = c->hctl->ack_entry;
+  s->progress_task = c->hctl->progress_task;
+  s->progress_entry = c->hctl->progress_entry;
+  s->signal = c->hctl->signal;
+  s->ack_ns = c->hctl->ack_ns;
+  return FP_OK;
+}
+
+int fp_task_logits(fp_ctx* c, fp_task* task, float* host_out) {
+  Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && t && host_out, "null argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(host_out, t->logits, (size_t)t->n_seqs * c->cfg.vocab * 4,
+                cudaMemcpyDeviceToHost));
+  return FP_OK;
+}
+
+int fp_task_read_kv(fp_ctx* c, fp_task* task, int32_t seq, int32_t layer, void* hk, void* hv) {
+  Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && t && hk && hv, "null argument");
+  REQ(seq >= 0 && seq < t->n_seqs && layer >= 0 && layer < c->cfg.num_layers, "bad seq/layer");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  const int PS = c->page_size, H = c->cfg.n_kv_heads, n = t->lens[seq];
+  int page_base = 0;
+  for (int i = 0; i < seq; ++i) page_base += (t->lens[i] + PS - 1) / PS;
+  std::vector<__nv_bfloat16> page((size_t)c->page_elems);
+  __nv_bfloat16* ok = static_cast<__nv_bfloat16*>(hk);
+  __nv_bfloat16* ov = static_cast<__nv_bfloat16*>(hv);
+  const __nv_bfloat16* kvl = c->kv + (long long)layer * c->kv_pages * c->page_elems;
+  for (int j = 0; j * PS < n; ++j) {
+    const int pg = t->pages[page_base + j];
+    CK(cudaMemcpy(page.data(), kvl + (long long)pg * c->page_elems, c->page_elems * 2,
+                  cudaMemcpyDeviceToHost));
+    for (int s = 0; s < PS && j * PS + s < n; ++s)
+      for (int h = 0; h < H; ++h)
+        for (int kv = 0; kv < 2; ++kv) {
+          const __nv_bfloat16* src = page.data() + ((size_t)(kv * H + h) * PS + s) * 128;
+          __nv_bfloat16* dst = (kv ? ov : ok) + ((size_t)(j * PS + s) * H + h) * 128;
+          memcpy(dst, src, 256);
+        }
+  }
+  return FP_OK;
+}
+
+int fp_op_gemm(fp_ctx* c, int32_t epi, const void* A, const void* B, void* C, int32_t M,
+               int32_t N, int32_t K) {
+  REQ(c && A && B && C, "null argument");
+  REQ(M >= 1 && N % 256 == 0 && K % 64 == 0, "gemm: N%256 and K%64 required");
+  CK(cudaSetDevice(c->device));
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_map(&ta, A, M, K, 128))) return rc;
+  if ((rc = make_map(&tb, B, N, K, 256))) return rc;
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.out = C;
+  p.ldo = N;
+  p.resid = static_cast<__nv_bfloat16*>(C);
+  p.ldr = N;
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  if (epi == 0) launch_gemm<EPI_STORE_BF16>(c, ta, tb, p, c->stream);
+  else if (epi == 1) launch_gemm<EPI_STORE_F32>(c, ta, tb, p, c->stream);
+  else if (epi == 2) launch_gemm<EPI_RESID>(c, ta, tb, p, c->stream);
+  else return set_err(FP_ERR_ARG, "bad epilogue");
+  CK(cudaGetLastError());
+  return FP_OK;
+}
+
+int fp_op_rmsnorm(fp_ctx* c, const void* x, const void* gamma, void* out, int32_t M, int32_t d,
+                  float eps) {
+  REQ(c && x && gamma && out, "null argument");
+  CK(cudaSetDevice(c->device));
+  RmsParams r{};
+  r.M = M;
+  r.d = d;
+  r.src = static_cast<const __nv_bfloat16*>(x);
+  r.ld_src = d;
+  r.gamma = static_cast<const __nv_bfloat16*>(gamma);
+  r.out = static_cast<__nv_bfloat16*>(out);
+  r.ld_out = d;
+  r.eps = eps;
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  int rc = launch_rms(r, c->stream);
+  if (rc) return rc;
+  CK(cudaGetLastError());
+  return FP_OK;
+}
+
+}  // extern "C"
