@@ -1,0 +1,51 @@
+"""Model shapes of the BASELINE configs (public model-card values; weights are random-init)."""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    name: str
+    num_layers: int
+    hidden: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    ffn: int
+    vocab: int
+    rope_theta: float
+    rms_eps: float = 1e-5
+
+    @property
+    def qdim(self) -> int:
+        return self.n_heads * self.head_dim
+
+    @property
+    def kvdim(self) -> int:
+        return self.n_kv_heads * self.head_dim
+
+    def gemm_flops_per_token(self) -> float:
+        """2 * (qkv + o + gate_up + down) weights, per token per layer."""
+        d = self.hidden
+        w = d * (self.qdim + 2 * self.kvdim) + self.qdim * d + 2 * d * self.ffn + self.ffn * d
+        return 2.0 * w
+
+    def attn_flops(self, share: int, prefix: int) -> float:
+        """Causal attention FLOPs of one request share with a prefix, per layer:
+        QK^T and PV over the visible keys, 4 * qdim * sum_i (prefix + i)."""
+        return 4.0 * self.qdim * (share * prefix + share * (share + 1) / 2.0)
+
+    def kv_bytes_per_token(self) -> int:
+        return self.num_layers * 2 * self.kvdim * 2
+
+
+SHAPES = {
+    "tiny": ModelShape("tiny", 4, 512, 4, 2, 128, 1536, 8192, 1e4),
+    "llama3-8b": ModelShape("llama3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 5e5),
+    # configs[2] (independent instances); q/k-norm not modelled in this build
+    "qwen3-8b": ModelShape("qwen3-8b", 36, 4096, 32, 8, 128, 12288, 151936, 1e6, 1e-6),
+    # configs[3] (TP); QKV bias not modelled in this build
+    "qwen2.5-32b": ModelShape("qwen2.5-32b", 64, 5120, 40, 8, 128, 27648, 152064, 1e6, 1e-6),
+}

@@ -1,0 +1,134 @@
+"""GPU parity: the full preemptible forward pass through the C ABI vs the CPU fp32 oracle.
+
+Tolerance (bf16 path vs fp32 oracle; stated per BASELINE north_star): logits max-abs error
+<= LOGIT_ATOL_FRAC * max|logit| and KV max-abs error <= KV_ATOL_FRAC * max|kv|. GPU-vs-GPU
+comparisons (preempted vs straight, batched vs alone, chunked KV reuse) are bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import forward as F
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_ATOL_FRAC = 0.03
+KV_ATOL_FRAC = 0.02
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    shape = F.SHAPES["tiny"]
+    w = F.make_weights(shape, 1234)
+    ctx = PrefillContext(SHAPES["tiny"], kv_pages=512, page_size=128, max_pos=8192)
+    ctx.load_weights(w)
+    yield shape, w, ctx
+    ctx.close()
+
+
+def run_straight(ctx, tokens, chunk=None, gran="operator"):
+    t = ctx.create_task(tokens, chunk, gran)
+    t.begin_segment(0)
+    t.enqueue(0, t.n_entries)
+    ctx.sync()
+    st = t.poll()
+    assert st.state == 3 and st.cursor == t.n_entries
+    return t
+
+
+def rel_err(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-6))
+
+
+def test_golden_hf_logits(tiny, golden_dir):
+    shape, w, ctx = tiny
+    g = np.load(f"{golden_dir}/tiny_hf_logits.npz")
+    tokens = F.make_tokens(list(g["lens"]), shape.vocab, int(g["seed"]))
+    t = run_straight(ctx, tokens)
+    lg = t.logits()
+    e = rel_err(lg, g["logits"])
+    print("tiny GPU vs HF golden: max-abs/max", e)
+    assert e <= LOGIT_ATOL_FRAC
+    t.destroy()
+
+
+@pytest.mark.parametrize("lens,chunk", [([300], None), ([37, 130, 64, 201], None),
+                                        ([37, 130, 64, 201], 100), ([1000, 5], 256)])
+def test_logits_and_kv_vs_oracle(tiny, lens, chunk):
+    shape, w, ctx = tiny
+    tokens = F.make_tokens(lens, shape.vocab, 77)
+    ot = F.OracleTask(shape, w, tokens, chunk)
+    ot.run_all()
+    t = run_straight(ctx, tokens, chunk)
+    lg = t.logits()
+    e = rel_err(lg, ot.logits)
+    print(f"lens={lens} chunk={chunk}: logits rel err {e:.4g}")
+    assert e <= LOGIT_ATOL_FRAC
+    for r in range(len(lens)):
+        for layer in (0, shape.num_layers - 1):
+            k, v = t.read_kv(r, layer)
+            ek = rel_err(k, ot.k_cache[r][layer])
+            ev = rel_err(v, ot.v_cache[r][layer])
+            assert ek <= KV_ATOL_FRAC and ev <= KV_ATOL_FRAC, (r, layer, ek, ev)
+    t.destroy()
+
+
+def test_batch_and_chunk_invariance_bitwise(tiny):
+    """Per-request results do not depend on batch composition (row-independent GEMMs,
+    per-request attention with absolute-position KV tiles)."""
+    shape, w, ctx = tiny
+    tokens = F.make_tokens([200, 90, 333], shape.vocab, 5)
+    batched = run_straight(ctx, tokens)
+    lb = batched.logits()
+    for r in range(3):
+        alone = run_straight(ctx, [tokens[r]])
+        assert np.array_equal(alone.logits()[0], lb[r])
+        alone.destroy()
+    batched.destroy()
+
+
+@pytest.mark.parametrize("gran", ["operator", "layer", "chunk"])
+def test_preemption_bitwise_and_cursor(tiny, gran):
+    """Stop at device boundary checks, resume from the published cursor: same bits as a
+    straight run, and stops only land on eligible boundaries."""
+    shape, w, ctx = tiny
+    tokens = F.make_tokens([257, 64], shape.vocab, 9)
+    chunk = 128 if gran == "chunk" else None
+    ref = run_straight(ctx, tokens, chunk, gran)
+    lref = ref.logits()
+    ref.destroy()
+    t = ctx.create_task(tokens, chunk, gran)
+    n = t.n_entries
+    rng = np.random.default_rng(0)
+    cursor, stops = 0, 0
+    while True:
+        t.begin_segment(cursor)
+        run_to = min(n, cursor + int(rng.integers(1, 12)))
+        t.enqueue(cursor, run_to)
+        ctx.sync()
+        if run_to == n:
+            break
+        ctx.signal()
+        t.enqueue(run_to, n)  # the rest of the task is queued behind the signal
+        ctx.sync()
+        st = t.poll()
+        if st.state != 2:  # no eligible boundary left: the task ran to completion
+            assert st.state == 3
+            ctx.clear()
+            break
+        stops += 1
+        assert st.cursor >= run_to
+        prev = st.cursor - 1  # last executed entry; the boundary after it must be eligible
+        if gran == "layer":
+            assert prev % 5 == 4
+        if gran == "chunk":
+            assert prev % (5 * shape.num_layers) == 5 * shape.num_layers - 1
+        assert ctx.poll().signal == 0  # the device unset the flag when it stopped
+        cursor = st.cursor
+    assert stops > 0
+    assert t.poll().state == 3
+    assert np.array_equal(t.logits(), lref)
+    t.destroy()
