@@ -119,6 +119,11 @@ int fp_task_create(fp_ctx* ctx, const int32_t* token_ids, const int32_t* seq_len
                    int32_t n_seqs, int32_t chunk_tokens, int32_t granularity, int32_t task_id,
                    fp_task** out);
 int fp_task_num_entries(const fp_task* task);
+typedef struct fp_task_info {
+  int32_t n_entries, n_chunks, n_seqs, total_tokens, max_chunk_tokens, n_pages;
+  int64_t upload_bytes; /* host->device bytes copied by fp_task_create (ids + plan) */
+} fp_task_info_t;
+int fp_task_info(const fp_task* task, fp_task_info_t* info);
 int fp_task_entry_info(const fp_task* task, int32_t entry, int32_t* chunk, int32_t* layer,
                        int32_t* op, int32_t* new_tokens);
 int fp_task_destroy(fp_ctx* ctx, fp_task* task);
@@ -143,6 +148,30 @@ int fp_poll(fp_ctx* ctx, fp_status* out);
 int fp_task_logits(fp_ctx* ctx, fp_task* task, float* host_out); /* [n_seqs, vocab] */
 int fp_task_read_kv(fp_ctx* ctx, fp_task* task, int32_t seq, int32_t layer, void* host_k,
                     void* host_v); /* each [seq_len, n_kv_heads, head_dim] bf16 */
+
+/* ---- live kernel profiling (CUDA events around every kernel on the prefill stream) ---- */
+#define FP_K_RMS 0
+#define FP_K_QKV 1
+#define FP_K_ATTN 2
+#define FP_K_O 3
+#define FP_K_GATE_UP 4
+#define FP_K_DOWN 5
+#define FP_K_LM_HEAD 6
+#define FP_K_RMS_FINAL 7
+typedef struct fp_prof_rec {
+  int32_t kind;  /* FP_K_* */
+  int32_t layer;
+  int32_t M;     /* token rows of the launch */
+  int32_t pad;
+  double flops;  /* algorithmic FLOPs of the launch (0 for HBM-bound kernels) */
+  double bytes;  /* algorithmic HBM bytes of the launch (0 for tensor-bound kernels) */
+  double ms;     /* event-measured duration */
+} fp_prof_rec;
+int fp_prof_enable(fp_ctx* ctx, int32_t on);
+/* Synchronises, returns up to max records (n = total recorded) and clears the log. */
+int fp_prof_collect(fp_ctx* ctx, fp_prof_rec* out, int32_t max, int32_t* n);
+/* Number of kernels this context has launched (guarded no-ops included). */
+int fp_ctx_launch_count(fp_ctx* ctx, int64_t* n);
 
 /* ---- per-operator entry points (device pointers; unit tests and microbenchmarks) -------- */
 /* C[M,N] = A[M,K] B[N,K]^T; epi: 0 bf16 store, 1 fp32 store, 2 residual add into C (bf16). */

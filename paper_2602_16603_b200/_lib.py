@@ -62,6 +62,33 @@ class TaskStatus(C.Structure):
     ]
 
 
+class TaskInfo(C.Structure):
+    _fields_ = [
+        ("n_entries", C.c_int32),
+        ("n_chunks", C.c_int32),
+        ("n_seqs", C.c_int32),
+        ("total_tokens", C.c_int32),
+        ("max_chunk_tokens", C.c_int32),
+        ("n_pages", C.c_int32),
+        ("upload_bytes", C.c_int64),
+    ]
+
+
+class ProfRec(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("layer", C.c_int32),
+        ("M", C.c_int32),
+        ("pad", C.c_int32),
+        ("flops", C.c_double),
+        ("bytes", C.c_double),
+        ("ms", C.c_double),
+    ]
+
+
+KERNEL_KINDS = ("rmsnorm", "qkv_gemm", "attn", "o_gemm", "gate_up_gemm", "down_gemm",
+                "lm_head_gemm", "final_rmsnorm")
+
 # name -> (restype, argtypes)
 _P = C.c_void_p
 _I = C.c_int32
@@ -78,6 +105,7 @@ _SIGS = {
     "fp_weights_load": (C.c_int, [_P, _I, _I, _P, C.c_int64]),
     "fp_task_create": (C.c_int, [_P, _P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
     "fp_task_num_entries": (C.c_int, [_P]),
+    "fp_task_info": (C.c_int, [_P, C.POINTER(TaskInfo)]),
     "fp_task_entry_info": (C.c_int, [_P, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "fp_task_destroy": (C.c_int, [_P, _P]),
     "fp_task_begin_segment": (C.c_int, [_P, _P, _I]),
@@ -89,6 +117,9 @@ _SIGS = {
     "fp_poll": (C.c_int, [_P, C.POINTER(Status)]),
     "fp_task_logits": (C.c_int, [_P, _P, _P]),
     "fp_task_read_kv": (C.c_int, [_P, _P, _I, _I, _P, _P]),
+    "fp_prof_enable": (C.c_int, [_P, _I]),
+    "fp_prof_collect": (C.c_int, [_P, C.POINTER(ProfRec), _I, C.POINTER(_I)]),
+    "fp_ctx_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "fp_op_gemm": (C.c_int, [_P, _I, _P, _P, _P, _I, _I, _I]),
     "fp_op_rmsnorm": (C.c_int, [_P, _P, _P, _P, _I, _I, C.c_float]),
 }

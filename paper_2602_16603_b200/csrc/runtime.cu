@@ -101,6 +101,7 @@ struct ChunkPlan {
   int tok0;       // first token of the chunk in the task's concatenated stream
   int item0, n_items;
   int last0, n_last, seq0;  // requests completing in this chunk: rows at last_rows[last0..]
+  double attn_flops;        // causal QK^T + PV FLOPs of the chunk (per layer)
 };
 
 struct Task {
@@ -110,6 +111,7 @@ struct Task {
   std::vector<ChunkPlan> chunks;
   std::vector<int> pages;  // KV pages owned
   int bt_stride = 0;
+  long long upload_bytes = 0;
   // device
   char* meta = nullptr;  // one allocation: ids | pos | tok_page | items | bt | last_rows
   int *d_ids, *d_pos, *d_tpage, *d_bt, *d_last;
@@ -149,6 +151,55 @@ struct fp_ctx {
   Task* wtask = nullptr;
   bool wquit = false;
   int window = 8;
+  // pinned staging arena for task uploads
+  std::mutex stage_mu;
+  char* stage = nullptr;
+  size_t stage_cap = 0;
+  cudaEvent_t stage_ev = nullptr;
+  // live per-kernel profiling (CUDA events on the prefill stream) and launch counting
+  bool prof_on = false;
+  std::vector<fp_prof_rec> prof_meta;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+  std::vector<cudaEvent_t> ev_pool;
+  std::atomic<long long> launches{0};
+};
+
+static cudaEvent_t ev_get(fp_ctx* c) {
+  if (c->ev_pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = c->ev_pool.back();
+  c->ev_pool.pop_back();
+  return e;
+}
+struct ProfScope {
+  fp_ctx* c;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  fp_prof_rec rec{};
+  ProfScope(fp_ctx* c_, cudaStream_t st_, int kind, int layer, int M, double flops, double bytes)
+      : c(c_), st(st_) {
+    rec.kind = kind;
+    rec.layer = layer;
+    rec.M = M;
+    rec.flops = flops;
+    rec.bytes = bytes;
+    if (c->prof_on) {
+      a = ev_get(c);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    c->launches++;
+    if (c->prof_on) {
+      cudaEvent_t b = ev_get(c);
+      cudaEventRecord(b, st);
+      c->prof_meta.push_back(rec);
+      c->prof_ev.push_back({a, b});
+    }
+  }
 };
 
 // --------------------------------------------------------------------------- launches
@@ -249,8 +300,11 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
     r.ld_out = m.hidden;
     r.eps = m.rms_eps;
     r.guard = g;
-    int rc = launch_rms(r, st);
-    if (rc) return rc;
+    {
+      ProfScope ps(c, st, FP_K_RMS, layer, M, 0.0, (layer == 0 && op == 0 ? 3.0 : 2.0) * M * m.hidden * 2);
+      int rc = launch_rms(r, st);
+      if (rc) return rc;
+    }
     GemmParams p{};
     p.M = M;
     p.K = m.hidden;
@@ -267,11 +321,13 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
       p.kv_cols = c->kvdim;
       p.page_size = c->page_size;
       p.n_kv_heads = m.n_kv_heads;
+      ProfScope ps(c, st, FP_K_QKV, layer, M, 2.0 * M * p.N * p.K, 0.0);
       launch_gemm<EPI_QKV>(c, t->tm_xn, ly.tm_qkv, p, st);
     } else {
       p.N = 2 * m.ffn;
       p.out = t->act;
       p.ldo = m.ffn;
+      ProfScope ps(c, st, FP_K_GATE_UP, layer, M, 2.0 * M * p.N * p.K, 0.0);
       launch_gemm<EPI_SWIGLU>(c, t->tm_xn, ly.tm_gu, p, st);
     }
   } else if (op == FP_OP_ATTN) {
@@ -290,7 +346,10 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
     a.page_size = c->page_size;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)m.head_dim);
     a.guard = g;
-    if (a.n_items > 0) launch_attn(a, st);
+    if (a.n_items > 0) {
+      ProfScope ps(c, st, FP_K_ATTN, layer, M, ch.attn_flops, 0.0);
+      launch_attn(a, st);
+    }
   } else {  // O_PROJ / DOWN_PROJ: residual add
     GemmParams p{};
     p.M = M;
@@ -300,10 +359,14 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
     p.guard = g;
     if (op == FP_OP_O_PROJ) {
       p.K = c->qdim;
+      ProfScope ps(c, st, FP_K_O, layer, M, 2.0 * M * p.N * p.K, 0.0);
       launch_gemm<EPI_RESID>(c, t->tm_ao, ly.tm_o, p, st);
     } else {
       p.K = m.ffn;
-      launch_gemm<EPI_RESID>(c, t->tm_act, ly.tm_d, p, st);
+      {
+        ProfScope ps(c, st, FP_K_DOWN, layer, M, 2.0 * M * p.N * p.K, 0.0);
+        launch_gemm<EPI_RESID>(c, t->tm_act, ly.tm_d, p, st);
+      }
       if (layer == L - 1 && ch.n_last > 0) {  // completion: final norm + lm_head of last tokens
         RmsParams r{};
         r.M = ch.n_last;
@@ -316,8 +379,11 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
         r.ld_out = m.hidden;
         r.eps = m.rms_eps;
         r.guard = g2;
-        int rc = launch_rms(r, st);
-        if (rc) return rc;
+        {
+          ProfScope ps(c, st, FP_K_RMS_FINAL, layer, ch.n_last, 0.0, 2.0 * ch.n_last * m.hidden * 2);
+          int rc = launch_rms(r, st);
+          if (rc) return rc;
+        }
         GemmParams q{};
         q.M = ch.n_last;
         q.N = m.vocab;
@@ -325,6 +391,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
         q.out = t->logits + (long long)ch.seq0 * m.vocab;
         q.ldo = m.vocab;
         q.guard = g2;
+        ProfScope ps(c, st, FP_K_LM_HEAD, layer, ch.n_last, 2.0 * ch.n_last * q.N * q.K, 0.0);
         launch_gemm<EPI_STORE_F32>(c, t->tm_xf, c->tm_lm, q, st);
       }
     }
@@ -480,6 +547,8 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaFree(c->rope);
   cudaFree(c->kv);
   cudaFreeHost((void*)c->hctl);
+  if (c->stage) cudaFreeHost(c->stage);
+  if (c->stage_ev) cudaEventDestroy(c->stage_ev);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->upload);
   delete c;
@@ -673,6 +742,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
       if (share <= 0) continue;
       const long long prefix = std::min(std::max(s - r0, 0LL), (long long)lens[r]);
       const int row0 = (int)(std::max(s, r0) - s);
+      ch.attn_flops += 4.0 * c->qdim * ((double)share * prefix + (double)share * (share + 1) / 2.0);
       for (long long k = 0; k < share; k += 64) {
         AttnItem it;
         it.q_row0 = row0 + (int)k;
@@ -712,8 +782,24 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   const size_t o_ids = put(ids, n_ids * 4), o_pos = put(pos.data(), n_ids * 4),
                o_tp = put(tpage.data(), n_ids * 4), o_it = put(items.data(), n_items * sizeof(AttnItem)),
                o_bt = put(bt.data(), n_bt * 4), o_last = put(last_rows.data(), n_last * 4);
-  CK(cudaMalloc(&t->meta, o + 16));
-  CK(cudaMemcpy(t->meta, host.data(), o, cudaMemcpyHostToDevice));
+  // Stream-ordered allocation + upload on the upload stream, from a pinned staging arena, so
+  // building a task never waits behind the running task's kernels.
+  cudaStream_t up = c->upload;
+  {
+    std::lock_guard<std::mutex> lk(c->stage_mu);
+    if (c->stage_ev) CK(cudaEventSynchronize(c->stage_ev));  // previous upload drained
+    if (c->stage_cap < o) {
+      if (c->stage) cudaFreeHost(c->stage);
+      c->stage_cap = std::max<size_t>(o, 1 << 20);
+      CK(cudaHostAlloc(&c->stage, c->stage_cap, cudaHostAllocDefault));
+    }
+    memcpy(c->stage, host.data(), o);
+    CK(cudaMallocAsync((void**)&t->meta, o + 16, up));
+    CK(cudaMemcpyAsync(t->meta, c->stage, o, cudaMemcpyHostToDevice, up));
+    if (!c->stage_ev) CK(cudaEventCreateWithFlags(&c->stage_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->stage_ev, up));
+  }
+  t->upload_bytes = (long long)o;
   t->d_ids = reinterpret_cast<int*>(t->meta + o_ids);
   t->d_pos = reinterpret_cast<int*>(t->meta + o_pos);
   t->d_tpage = reinterpret_cast<int*>(t->meta + o_tp);
@@ -722,25 +808,40 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   t->d_last = reinterpret_cast<int*>(t->meta + o_last);
   // workspaces (resume state lives here: h + the live intermediate)
   const long long M = t->max_m, d = m.hidden;
-  CK(cudaMalloc(&t->h, M * d * 2));
-  CK(cudaMalloc(&t->xn, M * d * 2));
-  CK(cudaMalloc(&t->q, M * c->qdim * 2));
-  CK(cudaMalloc(&t->ao, M * c->qdim * 2));
-  CK(cudaMalloc(&t->act, M * (long long)m.ffn * 2));
-  CK(cudaMalloc(&t->xf, (long long)n_seqs * d * 2));
-  CK(cudaMalloc(&t->logits, (long long)n_seqs * m.vocab * 4));
-  CK(cudaMemset(t->logits, 0, (long long)n_seqs * m.vocab * 4));
+  CK(cudaMallocAsync((void**)&t->h, M * d * 2, up));
+  CK(cudaMallocAsync((void**)&t->xn, M * d * 2, up));
+  CK(cudaMallocAsync((void**)&t->q, M * c->qdim * 2, up));
+  CK(cudaMallocAsync((void**)&t->ao, M * c->qdim * 2, up));
+  CK(cudaMallocAsync((void**)&t->act, M * (long long)m.ffn * 2, up));
+  CK(cudaMallocAsync((void**)&t->xf, (long long)n_seqs * d * 2, up));
+  CK(cudaMallocAsync((void**)&t->logits, (long long)n_seqs * m.vocab * 4, up));
+  CK(cudaMemsetAsync(t->logits, 0, (long long)n_seqs * m.vocab * 4, up));
   const size_t ctl_bytes = sizeof(TaskCtl) + (size_t)t->n_entries * 4;
-  CK(cudaMalloc(&t->ctl, ctl_bytes));
-  CK(cudaMemset(t->ctl, 0, ctl_bytes));
-  CK(cudaMemset(&t->ctl->stopped_gen, 0xFF, 4));  // -1
+  CK(cudaMallocAsync((void**)&t->ctl, ctl_bytes, up));
+  CK(cudaMemsetAsync(t->ctl, 0, ctl_bytes, up));
+  CK(cudaMemsetAsync(&t->ctl->stopped_gen, 0xFF, 4, up));  // -1
   int rc;
   if ((rc = make_map(&t->tm_xn, t->xn, M, d, 128))) return rc;
   if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
   if ((rc = make_map(&t->tm_act, t->act, M, m.ffn, 128))) return rc;
   if ((rc = make_map(&t->tm_xf, t->xf, n_seqs, d, 128))) return rc;
+  CK(cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming));
+  CK(cudaEventRecord(t->ready, up));
   CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
   *out = reinterpret_cast<fp_task*>(t);
+  return FP_OK;
+}
+
+int fp_task_info(const fp_task* task, fp_task_info_t* info) {
+  const Task* t = reinterpret_cast<const Task*>(task);
+  REQ(t && info, "null argument");
+  info->n_entries = t->n_entries;
+  info->n_chunks = (int)t->chunks.size();
+  info->n_seqs = t->n_seqs;
+  info->total_tokens = t->total;
+  info->max_chunk_tokens = t->max_m;
+  info->n_pages = (int)t->pages.size();
+  info->upload_bytes = t->upload_bytes;
   return FP_OK;
 }
 
@@ -766,16 +867,22 @@ int fp_task_destroy(fp_ctx* c, fp_task* task) {
   REQ(c, "null ctx");
   CK(cudaSetDevice(c->device));
   while (t->worker_active.load()) std::this_thread::yield();
-  CK(cudaStreamSynchronize(c->stream));
-  cudaFree(t->meta);
-  cudaFree(t->h);
-  cudaFree(t->xn);
-  cudaFree(t->q);
-  cudaFree(t->ao);
-  cudaFree(t->act);
-  cudaFree(t->xf);
-  cudaFree(t->logits);
-  cudaFree(t->ctl);
+  // stream-ordered frees behind any queued (no-op) launches of this task
+  cudaStream_t st = c->stream;
+  {
+    std::lock_guard<std::mutex> lk(c->launch_mu);
+    cudaStreamWaitEvent(st, t->ready, 0);
+    cudaFreeAsync(t->meta, st);
+    cudaFreeAsync(t->h, st);
+    cudaFreeAsync(t->xn, st);
+    cudaFreeAsync(t->q, st);
+    cudaFreeAsync(t->ao, st);
+    cudaFreeAsync(t->act, st);
+    cudaFreeAsync(t->xf, st);
+    cudaFreeAsync(t->logits, st);
+    cudaFreeAsync(t->ctl, st);
+  }
+  cudaEventDestroy(t->ready);
   cudaEventDestroy(t->done);
   {
     std::lock_guard<std::mutex> lk(c->page_mu);
@@ -789,13 +896,18 @@ int fp_task_begin_segment(fp_ctx* c, fp_task* task, int32_t first) {
   Task* t = reinterpret_cast<Task*>(task);
   REQ(c && t, "null argument");
   REQ(first >= 0 && first < t->n_entries, "segment start out of range");
-  REQ(!t->worker_active.load(), "task is already running");
+  // a stopped segment's launch worker exits on its own once it observes the ACK
+  for (int spin = 0; t->worker_active.load(); ++spin) {
+    if (spin > 20000000) return set_err(FP_ERR_STATE, "task is already running");
+    std::this_thread::yield();
+  }
   std::lock_guard<std::mutex> lk(c->launch_mu);
   t->gen += 1;
   t->seg_first = first;
   t->enq = first;
   t->done_recorded = 0;
   t->seg_ack0 = c->hctl->ack_seq;
+  CK(cudaStreamWaitEvent(c->stream, t->ready, 0));
   CK(cudaMemsetAsync(&t->ctl->dec[first], 0, (size_t)(t->n_entries - first) * 4, c->stream));
   return FP_OK;
 }
@@ -922,6 +1034,41 @@ int fp_task_read_kv(fp_ctx* c, fp_task* task, int32_t seq, int32_t layer, void* 
           memcpy(dst, src, 256);
         }
   }
+  return FP_OK;
+}
+
+int fp_prof_enable(fp_ctx* c, int32_t on) {
+  REQ(c, "null ctx");
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  c->prof_on = on != 0;
+  return FP_OK;
+}
+
+int fp_prof_collect(fp_ctx* c, fp_prof_rec* out, int32_t max, int32_t* n) {
+  REQ(c && n, "null argument");
+  CK(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  CK(cudaStreamSynchronize(c->stream));
+  const int cnt = (int)c->prof_meta.size();
+  *n = cnt;
+  for (int i = 0; i < cnt; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->prof_ev[i].first, c->prof_ev[i].second);
+    if (out && i < max) {
+      out[i] = c->prof_meta[i];
+      out[i].ms = ms;
+    }
+    c->ev_pool.push_back(c->prof_ev[i].first);
+    c->ev_pool.push_back(c->prof_ev[i].second);
+  }
+  c->prof_meta.clear();
+  c->prof_ev.clear();
+  return FP_OK;
+}
+
+int fp_ctx_launch_count(fp_ctx* c, int64_t* n) {
+  REQ(c && n, "null argument");
+  *n = c->launches.load();
   return FP_OK;
 }
 

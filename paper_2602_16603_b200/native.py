@@ -138,6 +138,28 @@ class PrefillContext:
     def set_window(self, entries: int) -> None:
         _lib.check(self.lib.fp_ctx_set_window(self.h, entries), "fp_ctx_set_window")
 
+    # -- live profiling -------------------------------------------------------------
+    def profile(self, on: bool) -> None:
+        _lib.check(self.lib.fp_prof_enable(self.h, 1 if on else 0), "fp_prof_enable")
+
+    def drain_profile(self, max_records: int = 1 << 20) -> list[dict]:
+        """Synchronise and return every kernel record since the last drain."""
+        buf = (_lib.ProfRec * max_records)()
+        n = C.c_int32()
+        _lib.check(self.lib.fp_prof_collect(self.h, buf, max_records, C.byref(n)),
+                   "fp_prof_collect")
+        out = []
+        for i in range(min(n.value, max_records)):
+            r = buf[i]
+            out.append({"kind": _lib.KERNEL_KINDS[r.kind], "layer": r.layer, "M": r.M,
+                        "flops": r.flops, "bytes": r.bytes, "ms": r.ms})
+        return out
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _lib.check(self.lib.fp_ctx_launch_count(self.h, C.byref(n)), "fp_ctx_launch_count")
+        return n.value
+
     def close(self) -> None:
         if self.h is not None:
             self.lib.fp_ctx_destroy(self.h)
@@ -176,6 +198,11 @@ class PrefillTask:
         )
         self.h = h
         self.n_entries = self.lib.fp_task_num_entries(h)
+
+    def info(self) -> dict:
+        inf = _lib.TaskInfo()
+        _lib.check(self.lib.fp_task_info(self.h, C.byref(inf)), "fp_task_info")
+        return {k: getattr(inf, k) for k, _ in _lib.TaskInfo._fields_}
 
     def entry_info(self, i: int) -> tuple[int, int, int, int]:
         c, l, o, n = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
