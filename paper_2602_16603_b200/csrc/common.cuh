@@ -117,6 +117,18 @@ DEVI void umma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]: A (M x K, 16-bit, two K elements per 32-bit column) read
+// from tensor memory -- used for P*V with P written by the softmax warps via tcgen05.st.
+DEVI void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Instruction descriptor, kind::f16: A=B=bf16, D=f32, both K-major unless b_mn_major.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool b_mn_major = false) {
   return (1u << 4)                       // D format f32
@@ -202,6 +214,11 @@ DEVI int ld_volatile_sys(const volatile int* p) {
   int v;
   asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+DEVI float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 DEVI uint64_t globaltimer() {
   uint64_t t;

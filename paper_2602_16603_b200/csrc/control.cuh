@@ -51,16 +51,31 @@ DEVI bool guard_pass(const Guard& g) {
   if (*sg == g.gen) return false;
   if (!g.first) return true;
   volatile int* slot = &g.task->dec[g.entry];
-  const int seen = *slot;  // most CTAs find the decision already made: no atomic needed
-  if (seen) return seen == kDecGo;
+  int d = *slot;  // most CTAs find the decision already made
+  if (d) return d == kDecGo;
+  // One decider per boundary: CTA 0 reads the pinned host flag (one PCIe read) and publishes
+  // the decision; the other CTAs wait for it in L2 instead of all hitting PCIe. A waiter that
+  // sees no decision for a long time takes the decider path itself (atomicCAS keeps it
+  // consistent), so progress never depends on CTA scheduling order.
+  bool decider = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  if (!decider) {
+    for (int spin = 0; spin < 200000; ++spin) {
+      d = *slot;
+      if (d) return d == kDecGo;
+      __nanosleep(32);
+    }
+    decider = true;
+  }
   int want = kDecGo;
   if (g.eligible && g.host != nullptr && ld_volatile_sys(&g.host->signal)) want = kDecStop;
   const int old = atomicCAS(&g.task->dec[g.entry], 0, want);
-  const int d = old ? old : want;
+  d = old ? old : want;
+  if (old == 0 && d == kDecStop) {  // later launches of this generation become no-ops
+    *sg = g.gen;                    // (they start only after this kernel has exited)
+    __threadfence();
+  }
   if (old == 0 && g.host != nullptr) {  // the winning CTA publishes the decision
     if (d == kDecStop) {
-      *sg = g.gen;
-      __threadfence();
       g.host->signal = 0;
       g.host->ack_task = g.task_id;
       g.host->ack_entry = g.entry;
@@ -73,9 +88,6 @@ DEVI bool guard_pass(const Guard& g) {
       g.host->progress_entry = g.entry;
       __threadfence_system();
     }
-  } else if (old == 0 && d == kDecStop) {
-    *sg = g.gen;
-    __threadfence();
   }
   return d == kDecGo;
 }

@@ -27,7 +27,7 @@ struct RmsParams {
 constexpr int kRmsRowsPerBlock = 8;
 
 template <int NV>  // d = NV * 256
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const RmsParams p) {
+__global__ void __launch_bounds__(256, 2) rmsnorm_kernel(const RmsParams p) {
   if (!guard_block(p.guard)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * kRmsRowsPerBlock + warp;

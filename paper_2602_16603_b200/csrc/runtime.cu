@@ -12,7 +12,7 @@
 #include <vector>
 
 #include "../../include/flowprefill.h"
-#include "attn_mma.cuh"
+#include "attn_tc.cuh"
 #include "common.cuh"
 #include "control.cuh"
 #include "gemm.cuh"
@@ -115,11 +115,11 @@ struct Task {
   // device
   char* meta = nullptr;  // one allocation: ids | pos | tok_page | items | bt | last_rows
   int *d_ids, *d_pos, *d_tpage, *d_bt, *d_last;
-  AttnItem* d_items;
+  AttnTile* d_items;
   __nv_bfloat16 *h, *xn, *q, *ao, *act, *xf;
   float* logits;
   TaskCtl* ctl;
-  CUtensorMap tm_xn, tm_ao, tm_act, tm_xf;
+  CUtensorMap tm_xn, tm_ao, tm_act, tm_xf, tm_q;
   cudaEvent_t ready, done;
   // host execution state
   int gen = 0, seg_first = 0, enq = 0, seg_ack0 = 0, done_recorded = 0;
@@ -134,6 +134,7 @@ struct fp_ctx {
   std::vector<Layer> layers;
   __nv_bfloat16 *embed = nullptr, *final_g = nullptr, *lm_head = nullptr;
   CUtensorMap tm_lm;
+  CUtensorMap tm_kv;  // paged KV pool as [L*P*2*Hkv*PS, 128] rows
   float2* rope = nullptr;
   __nv_bfloat16* kv = nullptr;
   long long page_elems = 0;  // elements of one page in one layer (2*Hkv*PS*hd)
@@ -233,15 +234,16 @@ static int launch_rms(const RmsParams& p, cudaStream_t st) {
   return FP_OK;
 }
 
-static void launch_attn(const AttnParams& p, cudaStream_t st) {
+static void launch_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const AttnTcParams& p,
+                        cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_prefill_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kAttnMmaSmem);
+    cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         tcattn::SMEM_BYTES);
     attr = true;
   }
-  dim3 grid(p.n_items, p.n_heads);
-  attn_prefill_mma_kernel<<<grid, mmaattn::THREADS, kAttnMmaSmem, st>>>(p);
+  dim3 grid(p.n_items, p.n_kv_heads * p.pairs_per_kv);
+  attn_prefill_tc_kernel<<<grid, tcattn::THREADS, tcattn::SMEM_BYTES, st>>>(tq, tkv, p);
 }
 
 static bool boundary_eligible(const fp_ctx* c, int gran, int i, int n_entries) {
@@ -331,24 +333,23 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
       launch_gemm<EPI_SWIGLU>(c, t->tm_xn, ly.tm_gu, p, st);
     }
   } else if (op == FP_OP_ATTN) {
-    AttnParams a{};
+    AttnTcParams a{};
     a.items = t->d_items + ch.item0;
     a.n_items = ch.n_items;
     a.n_heads = m.n_heads;
-    a.q = t->q;
-    a.ldq = c->qdim;
+    a.n_kv_heads = m.n_kv_heads;
+    a.pairs_per_kv = (m.n_heads / m.n_kv_heads + 1) / 2;
     a.out = t->ao;
     a.ldo = c->qdim;
-    a.kv_layer = kv_layer;
     a.block_table = t->d_bt;
     a.bt_stride = t->bt_stride;
-    a.n_kv_heads = m.n_kv_heads;
-    a.page_size = c->page_size;
+    a.kv_row_layer = (long long)layer * c->kv_pages * 2 * m.n_kv_heads * c->page_size;
+    a.kv_rows_per_page = 2 * m.n_kv_heads * c->page_size;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)m.head_dim);
     a.guard = g;
     if (a.n_items > 0) {
       ProfScope ps(c, st, FP_K_ATTN, layer, M, ch.attn_flops, 0.0);
-      launch_attn(a, st);
+      launch_attn(t->tm_q, c->tm_kv, a, st);
     }
   } else {  // O_PROJ / DOWN_PROJ: residual add
     GemmParams p{};
@@ -452,7 +453,7 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   REQ(cfg->n_heads % cfg->n_kv_heads == 0, "n_heads must be a multiple of n_kv_heads");
   REQ(((cfg->n_heads + 2 * cfg->n_kv_heads) * 128) % 256 == 0, "qkv width must be %256");
   REQ(cfg->vocab % 256 == 0, "vocab must be a multiple of 256");
-  REQ(page_size > 0 && page_size % 64 == 0, "page_size must be a multiple of 64");
+  REQ(page_size == 128, "page_size must be 128 (one attention KV tile per page)");
   REQ(kv_pages > 0, "kv_pages must be > 0");
   CK(cudaSetDevice(device));
   int major = 0;
@@ -512,6 +513,15 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     CK(cudaMemcpy(c->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   }
   CK(cudaMalloc(&c->kv, (size_t)L * kv_pages * c->page_elems * 2));
+  // zero once: slots past a request's length are read (and masked) by attention tiles, so
+  // they must hold finite values
+  CK(cudaMemset(c->kv, 0, (size_t)L * kv_pages * c->page_elems * 2));
+  {
+    const uint64_t rows = (uint64_t)L * kv_pages * 2 * cfg->n_kv_heads * page_size;
+    REQ(rows < (1ull << 31), "KV pool too large for 32-bit TMA row coordinates");
+    int rc = make_map(&c->tm_kv, c->kv, rows, 128, 128);
+    if (rc) return rc;
+  }
   c->free_pages.resize(kv_pages);
   for (long long i = 0; i < kv_pages; ++i) c->free_pages[i] = (int)(kv_pages - 1 - i);
   CK(cudaHostAlloc(&c->hctl, sizeof(HostCtl), cudaHostAllocMapped));
@@ -721,7 +731,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
     for (long long lo = 0; lo < total; lo += chunk_tokens)
       bounds.push_back({lo, std::min(lo + chunk_tokens, total)});
   std::vector<int> pos(total), tpage(total), last_rows;
-  std::vector<AttnItem> items;
+  std::vector<AttnTile> items;
   for (int i = 0; i < n_seqs; ++i)
     for (int p = 0; p < lens[i]; ++p) {
       pos[starts[i] + p] = p;
@@ -735,7 +745,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
     ch.item0 = (int)items.size();
     ch.last0 = (int)last_rows.size();
     ch.seq0 = -1;
-    std::vector<AttnItem> its;
+    std::vector<AttnTile> its;
     for (int r = 0; r < n_seqs; ++r) {
       const long long r0 = starts[r], r1 = starts[r + 1];
       const long long share = std::min(e, r1) - std::max(s, r0);
@@ -743,10 +753,10 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
       const long long prefix = std::min(std::max(s - r0, 0LL), (long long)lens[r]);
       const int row0 = (int)(std::max(s, r0) - s);
       ch.attn_flops += 4.0 * c->qdim * ((double)share * prefix + (double)share * (share + 1) / 2.0);
-      for (long long k = 0; k < share; k += 64) {
-        AttnItem it;
+      for (long long k = 0; k < share; k += 128) {
+        AttnTile it;
         it.q_row0 = row0 + (int)k;
-        it.n_rows = (int)std::min(64LL, share - k);
+        it.n_rows = (int)std::min(128LL, share - k);
         it.q_pos0 = (int)(prefix + k);
         it.req = r;
         its.push_back(it);
@@ -756,7 +766,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
         last_rows.push_back((int)(r1 - 1 - s));
       }
     }
-    std::stable_sort(its.begin(), its.end(), [](const AttnItem& a, const AttnItem& b) {
+    std::stable_sort(its.begin(), its.end(), [](const AttnTile& a, const AttnTile& b) {
       return a.q_pos0 + a.n_rows > b.q_pos0 + b.n_rows;  // longest KV range first
     });
     items.insert(items.end(), its.begin(), its.end());
@@ -769,7 +779,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   t->n_entries = (int)t->chunks.size() * m.num_layers * 5;
   // device metadata, one allocation
   const size_t n_ids = total, n_items = items.size(), n_bt = bt.size(), n_last = last_rows.size();
-  const size_t bytes = (3 * n_ids + n_bt + n_last) * 4 + n_items * sizeof(AttnItem) + 64;
+  const size_t bytes = (3 * n_ids + n_bt + n_last) * 4 + n_items * sizeof(AttnTile) + 64;
   std::vector<char> host(bytes, 0);
   size_t o = 0;
   auto put = [&](const void* src, size_t nb) {
@@ -780,7 +790,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   };
   host.resize(bytes + 6 * 16);
   const size_t o_ids = put(ids, n_ids * 4), o_pos = put(pos.data(), n_ids * 4),
-               o_tp = put(tpage.data(), n_ids * 4), o_it = put(items.data(), n_items * sizeof(AttnItem)),
+               o_tp = put(tpage.data(), n_ids * 4), o_it = put(items.data(), n_items * sizeof(AttnTile)),
                o_bt = put(bt.data(), n_bt * 4), o_last = put(last_rows.data(), n_last * 4);
   // Stream-ordered allocation + upload on the upload stream, from a pinned staging arena, so
   // building a task never waits behind the running task's kernels.
@@ -803,7 +813,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   t->d_ids = reinterpret_cast<int*>(t->meta + o_ids);
   t->d_pos = reinterpret_cast<int*>(t->meta + o_pos);
   t->d_tpage = reinterpret_cast<int*>(t->meta + o_tp);
-  t->d_items = reinterpret_cast<AttnItem*>(t->meta + o_it);
+  t->d_items = reinterpret_cast<AttnTile*>(t->meta + o_it);
   t->d_bt = reinterpret_cast<int*>(t->meta + o_bt);
   t->d_last = reinterpret_cast<int*>(t->meta + o_last);
   // workspaces (resume state lives here: h + the live intermediate)
@@ -825,6 +835,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
   if ((rc = make_map(&t->tm_act, t->act, M, m.ffn, 128))) return rc;
   if ((rc = make_map(&t->tm_xf, t->xf, n_seqs, d, 128))) return rc;
+  if ((rc = make_map(&t->tm_q, t->q, M, c->qdim, 128))) return rc;
   CK(cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming));
   CK(cudaEventRecord(t->ready, up));
   CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
