@@ -221,16 +221,10 @@ static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
 }
 
 static int launch_rms(const RmsParams& p, cudaStream_t st) {
-  const int grid = (p.M + kRmsRowsPerBlock - 1) / kRmsRowsPerBlock;
-  if (grid == 0) return FP_OK;
-  switch (p.d / 256) {
-    case 2: rmsnorm_kernel<2><<<grid, 256, 0, st>>>(p); break;
-    case 4: rmsnorm_kernel<4><<<grid, 256, 0, st>>>(p); break;
-    case 8: rmsnorm_kernel<8><<<grid, 256, 0, st>>>(p); break;
-    case 16: rmsnorm_kernel<16><<<grid, 256, 0, st>>>(p); break;
-    case 20: rmsnorm_kernel<20><<<grid, 256, 0, st>>>(p); break;
-    default: return set_err(FP_ERR_UNSUPPORTED, "rmsnorm: unsupported hidden size");
-  }
+  if (p.M == 0) return FP_OK;
+  if (p.d % 256 != 0 || p.d > 8192)
+    return set_err(FP_ERR_UNSUPPORTED, "rmsnorm: hidden size must be a multiple of 256, <= 8192");
+  rmsnorm_kernel<<<p.M, p.d / 8, 0, st>>>(p);
   return FP_OK;
 }
 
