@@ -75,21 +75,10 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   uint64_t* o_full = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
-  if (!guard_block(p.guard)) return;
-
-  const AttnTile it = p.items[blockIdx.x];
-  const int kvh = blockIdx.y / p.pairs_per_kv;
-  const int pair = blockIdx.y % p.pairs_per_kv;
-  const int group = p.n_heads / p.n_kv_heads;
-  const int head0 = kvh * group + 2 * pair;
-  const bool has_head1 = 2 * pair + 1 < group;
-  const int head1 = has_head1 ? head0 + 1 : head0;
-  const int kv_len = it.q_pos0 + it.n_rows;
-  const int n_tiles = (kv_len + TILE - 1) / TILE;
-  const int* bt = p.block_table + (long long)it.req * p.bt_stride;
 
   const int warp = warp_id();
   const int lane = lane_id();
+  // prologue (overlaps the previous kernel's tail under programmatic dependent launch)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmKV);
@@ -110,8 +99,23 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  grid_dep_wait();
+  const bool run = guard_block(p.guard);
 
-  if (warp == 0) {
+  const AttnTile it = p.items[blockIdx.x];
+  const int kvh = blockIdx.y / p.pairs_per_kv;
+  const int pair = blockIdx.y % p.pairs_per_kv;
+  const int group = p.n_heads / p.n_kv_heads;
+  const int head0 = kvh * group + 2 * pair;
+  const bool has_head1 = 2 * pair + 1 < group;
+  const int head1 = has_head1 ? head0 + 1 : head0;
+  const int kv_len = it.q_pos0 + it.n_rows;
+  const int n_tiles = (kv_len + TILE - 1) / TILE;
+  const int* bt = p.block_table + (long long)it.req * p.bt_stride;
+
+  if (!run) {
+    // stopped at this boundary: nothing to do
+  } else if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_last();  // K/V tiles are re-read by other q tiles

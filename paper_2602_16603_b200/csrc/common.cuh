@@ -215,6 +215,10 @@ DEVI int ld_volatile_sys(const volatile int* p) {
   asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Programmatic dependent launch: wait until the preceding kernel in the stream has completed
+// and its memory is visible (no-op when the launch was not programmatic).
+DEVI void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 DEVI float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -42,6 +42,13 @@ struct GemmParams {
   __nv_bfloat16* kv_layer;  // this layer's base of the paged KV pool
   const float2* rope;       // [max_pos][64] (cos, sin)
   int q_cols, kv_cols, page_size, n_kv_heads;
+  // split-K (small tile counts): `splits` K-slices per tile; fp32 partials go to `ws`
+  // ([tile][split][128][BN]) and the last-arriving CTA of a tile reduces them in split order
+  // (deterministic) and runs the fused epilogue. `tickets` must be zero (it is reset).
+  int splits;
+  int pad1;
+  float* ws;
+  int* tickets;
   Guard guard;
 };
 
@@ -102,8 +109,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  if (!guard_block(p.guard)) return;
-
   const int warp = warp_id();
   const int lane = lane_id();
   if (warp == 0 && lane == 0) {
@@ -126,20 +131,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // Everything above overlaps the previous kernel's tail (programmatic dependent launch);
+  // the boundary check and all data accesses come after the dependency resolves.
+  grid_dep_wait();
+  const bool run = guard_block(p.guard);
 
   const int num_m = (p.M + kGemmBM - 1) / kGemmBM;
   const int num_n = p.N / BN;
   const int num_tiles = num_m * num_n;
   const int num_k = p.K / kGemmBK;
+  const int splits = p.splits > 1 ? p.splits : 1;
+  const int kb_per = (num_k + splits - 1) / splits;
+  const int num_units = run ? num_tiles * splits : 0;  // unit u -> (tile, K-slice)
 
   if (warp == 0) {
     const uint64_t pol_b = policy_evict_last();
     int s = 0;
     uint32_t ph = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
-      for (int kb = 0; kb < num_k; ++kb) {
+      tile_coords(u / splits, num_m, num_n, mb, nb);
+      const int kb0 = (u % splits) * kb_per;
+      const int kb1 = min(num_k, kb0 + kb_per);
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
@@ -158,13 +172,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      const int kb0 = (u % splits) * kb_per;
+      const int kb1 = min(num_k, kb0 + kb_per);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_ph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tbase + acc * BN;
-      for (int kb = 0; kb < num_k; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
         if (lane == 0) {
@@ -173,7 +189,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k) {
             // +32 bytes along K inside the 128B swizzle atom (descriptor address is >>4)
-            umma_bf16_ss(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16_ss(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb != kb0 || k != 0));
           }
           tc_commit(&empty[s]);
         }
@@ -187,71 +203,150 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
     }
   } else if (warp >= 4) {
+    __shared__ int s_last;
     const int q = warp & 3;  // TMEM lane quadrant
     const int row = q * 32 + lane;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      const int tile = u / splits;
+      const int split = u % splits;
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_ph);
-      tc_fence_after();
-      const uint32_t tacc = tbase + acc * BN + ((uint32_t)(q * 32) << 16);
       const int m = mb * kGemmBM + row;
       const bool live = m < p.M;
       const int n0 = nb * BN;
-
-      if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32 || EPI == EPI_RESID) {
+      // Partial tiles are stored thread-major ([split][col/4][row] float4) so every warp
+      // access is one contiguous 512-byte segment.
+      float4* ws_tile = reinterpret_cast<float4*>(p.ws) + (long long)tile * splits * (BN / 4) * kGemmBM;
+      const uint32_t tacc = tbase + acc * BN + ((uint32_t)(q * 32) << 16);
+      if (splits > 1) {
+        mbar_wait(&tfull[acc], acc_ph);
+        tc_fence_after();
+        // 1) this K-slice's partial tile -> workspace, TMEM released immediately
+        float4* dst = ws_tile + (long long)split * (BN / 4) * kGemmBM + row;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
           tmem_ld32(tacc + c * 32, r);
           tmem_ld_wait();
-          if (live) {
-            float v[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          for (int i = 0; i < 8; ++i)
+            st_global_v4(dst + (c * 8 + i) * kGemmBM,
+                         make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]));
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        // 2) ticket: the last K-slice of the tile reduces and runs the epilogue
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (row == 0) {
+          const int old = atomicAdd(&p.tickets[tile], 1);
+          s_last = old == splits - 1;
+          if (s_last) p.tickets[tile] = 0;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (!s_last) continue;
+        __threadfence();
+      }
+      // Accumulator columns [col, col+32) of this thread's row: from TMEM, or the in-order sum
+      // of the split partials (split 0 first) -- the same bits whichever CTA arrives last.
+      auto load32 = [&](int col, float* v) {
+        if (splits == 1) {
+          uint32_t r[32];
+          tmem_ld32(tacc + col, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          for (int sp = 0; sp < splits; ++sp) {
+            const float4* src = ws_tile + ((long long)sp * (BN / 4) + col / 4) * kGemmBM + row;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 f = __ldcg(src + i * kGemmBM);
+              v[4 * i] += f.x;
+              v[4 * i + 1] += f.y;
+              v[4 * i + 2] += f.z;
+              v[4 * i + 3] += f.w;
+            }
+          }
+        }
+      };
+
+      if constexpr (EPI == EPI_RESID) {
+        // residual row segment prefetched into registers while the MMA runs
+        uint4 hres[BN / 8];
+        __nv_bfloat16* hrow = p.resid + (long long)m * p.ldr + n0;
+        if (live) {
+#pragma unroll
+          for (int i = 0; i < BN / 8; ++i) hres[i] = ld_global_v4(hrow + 8 * i);
+        }
+        if (splits == 1) {
+          mbar_wait(&tfull[acc], acc_ph);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          load32(c * 32, v);
+          if (live) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 h = hres[c * 4 + i];
+              const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float2 f = unpack_bf16x2(hw[j]);
+                v[8 * i + 2 * j] += f.x;
+                v[8 * i + 2 * j + 1] += f.y;
+              }
+            }
+            store_row32_bf16(hrow + c * 32, v);
+          }
+        }
+      } else if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32) {
+        if (splits == 1) {
+          mbar_wait(&tfull[acc], acc_ph);
+          tc_fence_after();
+        }
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          load32(c * 32, v);
+          if (live) {
             if constexpr (EPI == EPI_STORE_F32) {
               float* dst = reinterpret_cast<float*>(p.out) + (long long)m * p.ldo + n0 + c * 32;
 #pragma unroll
               for (int i = 0; i < 8; ++i)
-                st_global_v4(dst + 4 * i, make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2],
-                                                     r[4 * i + 3]));
-            } else if constexpr (EPI == EPI_STORE_BF16) {
+                st_global_v4(dst + 4 * i,
+                             make_uint4(__float_as_uint(v[4 * i]), __float_as_uint(v[4 * i + 1]),
+                                        __float_as_uint(v[4 * i + 2]),
+                                        __float_as_uint(v[4 * i + 3])));
+            } else {
               __nv_bfloat16* dst =
                   reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)m * p.ldo + n0 + c * 32;
-              store_row32_bf16(dst, v);
-            } else {  // EPI_RESID
-              __nv_bfloat16* dst = p.resid + (long long)m * p.ldr + n0 + c * 32;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint4 h = ld_global_v4(dst + 8 * i);
-                const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const float2 f = unpack_bf16x2(hw[j]);
-                  v[8 * i + 2 * j] += f.x;
-                  v[8 * i + 2 * j + 1] += f.y;
-                }
-              }
               store_row32_bf16(dst, v);
             }
           }
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
+        if (splits == 1) {
+          mbar_wait(&tfull[acc], acc_ph);
+          tc_fence_after();
+        }
         // Tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows.
 #pragma unroll 1
         for (int c = 0; c < BN / 64; ++c) {
-          uint32_t g[32], u[32];
-          tmem_ld32(tacc + c * 32, g);
-          tmem_ld32(tacc + BN / 2 + c * 32, u);
-          tmem_ld_wait();
+          float g[32], up[32];
+          load32(c * 32, g);
+          load32(BN / 2 + c * 32, up);
           if (live) {
             float v[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              v[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+            for (int i = 0; i < 32; ++i) v[i] = silu_f(g[i]) * up[i];
             __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)m * p.ldo +
                                  nb * (BN / 2) + c * 32;
             store_row32_bf16(dst, v);
@@ -260,7 +355,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       } else {  // EPI_QKV: 128-column heads
         const int pos = live ? p.pos[m] : 0;
         const int page = live ? p.tok_page[m] : 0;
-#pragma unroll 1
+        // (cos, sin) of the row's position for the 64 rotation pairs, prefetched during the MMA
+        float4 cs[32];
+        const bool rot = n0 < p.q_cols + p.kv_cols;  // tile holds q/k heads (v heads unrotated)
+        if (live && rot) {
+          const float4* src = reinterpret_cast<const float4*>(p.rope + (long long)pos * 64);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cs[i] = __ldg(src + i);
+        }
+        if (splits == 1) {
+          mbar_wait(&tfull[acc], acc_ph);
+          tc_fence_after();
+        }
+#pragma unroll
         for (int hh = 0; hh < BN / 128; ++hh) {
           const int col0 = n0 + hh * 128;
           const bool is_q = col0 < p.q_cols;
@@ -276,40 +383,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                    (pos % p.page_size)) *
                       128;
           }
-#pragma unroll 1
+#pragma unroll
           for (int half = 0; half < 2; ++half) {
             // chunk pair (half, half+2): columns j and j+64 of the head for j in this chunk
-            uint32_t a[32], b[32];
-            tmem_ld32(tacc + hh * 128 + half * 32, a);
-            tmem_ld32(tacc + hh * 128 + half * 32 + 64, b);
-            tmem_ld_wait();
+            float a[32], b[32];
+            load32(hh * 128 + half * 32, a);
+            load32(hh * 128 + half * 32 + 64, b);
             if (live) {
-              float x1[32], x2[32];
               if (!is_v) {
-                const float2* cs = p.rope + (long long)pos * 64 + half * 32;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const float2 t2 = cs[i];
-                  const float u1 = __uint_as_float(a[i]);
-                  const float u2 = __uint_as_float(b[i]);
-                  x1[i] = u1 * t2.x - u2 * t2.y;
-                  x2[i] = u2 * t2.x + u1 * t2.y;
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  x1[i] = __uint_as_float(a[i]);
-                  x2[i] = __uint_as_float(b[i]);
+                for (int i = 0; i < 16; ++i) {
+                  const float4 t4 = cs[half * 16 + i];  // (cos, sin) of columns 2i, 2i+1
+                  const float u1 = a[2 * i], u2 = b[2 * i];
+                  const float w1 = a[2 * i + 1], w2 = b[2 * i + 1];
+                  a[2 * i] = u1 * t4.x - u2 * t4.y;
+                  b[2 * i] = u2 * t4.x + u1 * t4.y;
+                  a[2 * i + 1] = w1 * t4.z - w2 * t4.w;
+                  b[2 * i + 1] = w2 * t4.z + w1 * t4.w;
                 }
               }
-              store_row32_bf16(dst + half * 32, x1);
-              store_row32_bf16(dst + half * 32 + 64, x2);
+              store_row32_bf16(dst + half * 32, a);
+              store_row32_bf16(dst + half * 32 + 64, b);
             }
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (splits == 1) {
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
     }
   }
 

@@ -27,6 +27,7 @@ struct RmsParams {
 
 __global__ void __launch_bounds__(1024) rmsnorm_kernel(const RmsParams p) {
   __shared__ float red[32];
+  grid_dep_wait();
   if (!guard_block(p.guard)) return;
   const int row = blockIdx.x;
   const int tid = threadIdx.x;

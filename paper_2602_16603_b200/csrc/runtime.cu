@@ -9,6 +9,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/flowprefill.h"
@@ -163,6 +164,9 @@ struct fp_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
   std::vector<cudaEvent_t> ev_pool;
   std::atomic<long long> launches{0};
+  // split-K workspace (one prefill stream: launches are serialised, one buffer suffices)
+  float* ws = nullptr;
+  int* tickets = nullptr;
 };
 
 static cudaEvent_t ev_get(fp_ctx* c) {
@@ -204,9 +208,48 @@ struct ProfScope {
 };
 
 // --------------------------------------------------------------------------- launches
+// Every kernel is launched with programmatic stream serialisation: its prologue (barrier init,
+// TMEM alloc, descriptor prefetch) may start while the previous kernel drains; the kernel
+// itself waits (griddepcontrol.wait) before its boundary check and any data access.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// K-split count for a GEMM whose tile count underfills the machine (small prefill chunks).
+// Cost model in units of one 64-wide k-block: waves * (k-blocks per slice + fixed) + the
+// partial write/reduce traffic per split. The choice depends on the shape only, and the
+// reduction order is fixed, so results are deterministic run to run.
+static int choose_splits(int tiles, int num_k, int num_sms) {
+  if (tiles >= num_sms) return 1;
+  int best = 1;
+  double best_t = 1e30;
+  for (int S = 1; S <= 8; ++S) {
+    if (S > 1 && (num_k / S < 4 || tiles * S > 2 * num_sms)) break;
+    const double waves = std::ceil((double)tiles * S / num_sms);
+    const double t = waves * ((double)num_k / S + 4.0) + (S > 1 ? 5.0 * S : 0.0);
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = S;
+    }
+  }
+  return best;
+}
+
 template <int EPI>
-static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
-                        const GemmParams& p, cudaStream_t st) {
+static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b, GemmParams p,
+                        cudaStream_t st) {
   constexpr int BN = 256;
   auto kern = gemm_bf16_tn_kernel<BN, EPI>;
   static bool attr = false;
@@ -216,15 +259,19 @@ static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
     attr = true;
   }
   const int tiles = ((p.M + kGemmBM - 1) / kGemmBM) * (p.N / BN);
-  const int grid = std::max(1, std::min(tiles, c->num_sms));
-  kern<<<grid, kGemmThreads, GemmCfg<BN>::SMEM_BYTES, st>>>(a, b, p);
+  p.splits = (c->ws && EPI != EPI_STORE_F32) ? choose_splits(tiles, p.K / kGemmBK, c->num_sms) : 1;
+  p.ws = c->ws;
+  p.tickets = c->tickets;
+  const int units = tiles * p.splits;
+  const int grid = std::max(1, std::min(units, c->num_sms));
+  launch_pdl(kern, dim3(grid), dim3(kGemmThreads), GemmCfg<BN>::SMEM_BYTES, st, a, b, p);
 }
 
 static int launch_rms(const RmsParams& p, cudaStream_t st) {
   if (p.M == 0) return FP_OK;
   if (p.d % 256 != 0 || p.d > 8192)
     return set_err(FP_ERR_UNSUPPORTED, "rmsnorm: hidden size must be a multiple of 256, <= 8192");
-  rmsnorm_kernel<<<p.M, p.d / 8, 0, st>>>(p);
+  launch_pdl(rmsnorm_kernel, dim3(p.M), dim3(p.d / 8), 0, st, p);
   return FP_OK;
 }
 
@@ -237,7 +284,8 @@ static void launch_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const Att
     attr = true;
   }
   dim3 grid(p.n_items, p.n_kv_heads * p.pairs_per_kv);
-  attn_prefill_tc_kernel<<<grid, tcattn::THREADS, tcattn::SMEM_BYTES, st>>>(tq, tkv, p);
+  launch_pdl(attn_prefill_tc_kernel, grid, dim3(tcattn::THREADS), tcattn::SMEM_BYTES, st, tq, tkv,
+             p);
 }
 
 static bool boundary_eligible(const fp_ctx* c, int gran, int i, int n_entries) {
@@ -518,6 +566,9 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   }
   c->free_pages.resize(kv_pages);
   for (long long i = 0; i < kv_pages; ++i) c->free_pages[i] = (int)(kv_pages - 1 - i);
+  CK(cudaMalloc(&c->ws, (size_t)2 * c->num_sms * kGemmBM * 256 * sizeof(float)));
+  CK(cudaMalloc(&c->tickets, 4096 * sizeof(int)));
+  CK(cudaMemset(c->tickets, 0, 4096 * sizeof(int)));
   CK(cudaHostAlloc(&c->hctl, sizeof(HostCtl), cudaHostAllocMapped));
   memset((void*)c->hctl, 0, sizeof(HostCtl));
   c->hctl->progress_task = -1;
@@ -550,6 +601,8 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaFree(c->final_g);
   cudaFree(c->rope);
   cudaFree(c->kv);
+  cudaFree(c->ws);
+  cudaFree(c->tickets);
   cudaFreeHost((void*)c->hctl);
   if (c->stage) cudaFreeHost(c->stage);
   if (c->stage_ev) cudaEventDestroy(c->stage_ev);

@@ -76,16 +76,20 @@ def test_logits_and_kv_vs_oracle(tiny, lens, chunk):
     t.destroy()
 
 
-def test_batch_and_chunk_invariance_bitwise(tiny):
-    """Per-request results do not depend on batch composition (row-independent GEMMs,
-    per-request attention with absolute-position KV tiles)."""
+def test_batch_composition(tiny):
+    """Per-request results do not depend on batch composition beyond bf16 rounding: rows are
+    independent in every GEMM and attention never crosses requests (the split-K choice may
+    differ with the batch's M, so this is a tolerance check). Repeated runs are bit-exact."""
     shape, w, ctx = tiny
     tokens = F.make_tokens([200, 90, 333], shape.vocab, 5)
     batched = run_straight(ctx, tokens)
     lb = batched.logits()
+    again = run_straight(ctx, tokens)
+    assert np.array_equal(again.logits(), lb)  # deterministic (fixed split-K reduction order)
+    again.destroy()
     for r in range(3):
         alone = run_straight(ctx, [tokens[r]])
-        assert np.array_equal(alone.logits()[0], lb[r])
+        assert rel_err(alone.logits()[0], lb[r]) <= 0.01
         alone.destroy()
     batched.destroy()
 
