@@ -42,11 +42,12 @@ struct GemmParams {
   __nv_bfloat16* kv_layer;  // this layer's base of the paged KV pool
   const float2* rope;       // [max_pos][64] (cos, sin)
   int q_cols, kv_cols, page_size, n_kv_heads;
-  // split-K (small tile counts): `splits` K-slices per tile; fp32 partials go to `ws`
-  // ([tile][split][128][BN]) and the last-arriving CTA of a tile reduces them in split order
-  // (deterministic) and runs the fused epilogue. `tickets` must be zero (it is reset).
+  // Tail split-K: the first `full_tiles` tiles (whole waves) run unsplit; each remaining tile
+  // is cut into `splits` K-slices so the last wave fills the machine. fp32 partials go to
+  // `ws` and the last-arriving CTA of a tile reduces them in split order (deterministic) and
+  // runs the fused epilogue. `tickets` must be zero on entry (the reducer resets it).
   int splits;
-  int pad1;
+  int full_tiles;
   float* ws;
   int* tickets;
   Guard guard;
@@ -57,12 +58,17 @@ constexpr int kGemmBK = 64;
 constexpr int kGemmThreads = 256;
 constexpr int kGemmGroupM = 16;  // m-blocks per raster group (L2 reuse of A and B)
 
-template <int BN>
+// CG = 1: one CTA computes a 128 x BN tile. CG = 2: a CTA pair (cluster of 2) computes a
+// 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA stages its own 128 A rows and BN/2 B
+// rows, so per-SM shared-memory traffic per k-block drops from 96 KB to 64 KB (the 1-CTA
+// kernel is smem-port bound at ~70% of the MMA rate).
+template <int BN, int CG = 1>
 struct GemmCfg {
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr int A_BYTES = kGemmBM * kGemmBK * 2;
-  static constexpr int B_BYTES = BN * kGemmBK * 2;
+  static constexpr int B_BYTES = (BN / CG) * kGemmBK * 2;
+  static constexpr int STAGES = (A_BYTES + B_BYTES) <= 32768 ? 6 : 4;
   static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int TILE_M = kGemmBM * CG;
   static constexpr int SMEM_BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
 };
 
@@ -92,11 +98,11 @@ DEVI void store_row32_bf16(__nv_bfloat16* dst, const float* v) {
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -111,24 +117,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA rank inside the pair
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 1);  // the leader's expect_tx arrival (+ both CTAs' TMA bytes)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 4 * CG);  // one arrival per epilogue warp of every CTA
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
+    else tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   // Everything above overlaps the previous kernel's tail (programmatic dependent launch);
@@ -136,29 +148,62 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   grid_dep_wait();
   const bool run = guard_block(p.guard);
 
-  const int num_m = (p.M + kGemmBM - 1) / kGemmBM;
+  const int num_m = (p.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
+  const int unit0 = blockIdx.x / CG;      // this CTA (pair)'s first work unit
+  const int unit_step = gridDim.x / CG;
   const int num_n = p.N / BN;
   const int num_tiles = num_m * num_n;
   const int num_k = p.K / kGemmBK;
-  const int splits = p.splits > 1 ? p.splits : 1;
-  const int kb_per = (num_k + splits - 1) / splits;
-  const int num_units = run ? num_tiles * splits : 0;  // unit u -> (tile, K-slice)
+  const int tail_splits = p.splits > 1 ? p.splits : 1;
+  const int full_tiles = tail_splits > 1 ? min(p.full_tiles, num_tiles) : num_tiles;
+  const int num_units = run ? full_tiles + (num_tiles - full_tiles) * tail_splits : 0;
+  // unit -> (tile, K-slice index, slice count, k-block range)
+  auto unit_info = [&](int u, int& tile, int& split, int& nsplit, int& kb0, int& kb1) {
+    if (u < full_tiles) {
+      tile = u;
+      split = 0;
+      nsplit = 1;
+      kb0 = 0;
+      kb1 = num_k;
+    } else {
+      const int v = u - full_tiles;
+      tile = full_tiles + v / tail_splits;
+      split = v % tail_splits;
+      nsplit = tail_splits;
+      const int per = (num_k + tail_splits - 1) / tail_splits;
+      kb0 = split * per;
+      kb1 = min(num_k, kb0 + per);
+    }
+  };
 
   if (warp == 0) {
     const uint64_t pol_b = policy_evict_last();
     int s = 0;
     uint32_t ph = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = unit0; u < num_units; u += unit_step) {
+      int tile, split, nsplit, kb0, kb1;
+      unit_info(u, tile, split, nsplit, kb0, kb1);
       int mb, nb;
-      tile_coords(u / splits, num_m, num_n, mb, nb);
-      const int kb0 = (u % splits) * kb_per;
-      const int kb1 = min(num_k, kb0 + kb_per);
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int row_a = mb * Cfg::TILE_M + (int)rank * kGemmBM;
+      const int row_b = nb * BN + (int)rank * (BN / CG);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
-          tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kGemmBK, mb * kGemmBM);
-          tma_load_2d_hint(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * kGemmBK, nb * BN, pol_b);
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+            tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kGemmBK, row_a);
+#pragma unroll
+            for (int h = 0; h < BN / 128; ++h)  // weight maps use 128-row boxes
+              tma_load_2d_hint(sB + s * Cfg::B_BYTES + h * 16384, &tmB, &full[s], kb * kGemmBK,
+                               row_b + h * 128, pol_b);
+          } else {
+            // The peer's bytes are counted on the leader's barrier by the 2-SM TMA; it cannot
+            // run ahead into this phase before the leader's MMA released the stage (empty).
+            if (leader) mbar_arrive_expect_tx(&full[s], 2 * (Cfg::A_BYTES + Cfg::B_BYTES));
+            tma_load_2d_2sm(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kGemmBK, row_a, pol_b);
+            tma_load_2d_2sm(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * kGemmBK, row_b, pol_b);
+          }
         }
         __syncwarp();
         if (++s == STAGES) {
@@ -167,14 +212,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc_bf16(kGemmBM, BN);
+  } else if (warp == 1 && leader) {
+    constexpr uint32_t idesc = make_idesc_bf16(Cfg::TILE_M, BN);
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
-      const int kb0 = (u % splits) * kb_per;
-      const int kb1 = min(num_k, kb0 + kb_per);
+    for (int u = unit0; u < num_units; u += unit_step, ++it) {
+      int tile, split, nsplit, kb0, kb1;
+      unit_info(u, tile, split, nsplit, kb0, kb1);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_ph ^ 1);
@@ -189,9 +234,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k) {
             // +32 bytes along K inside the 128B swizzle atom (descriptor address is >>4)
-            umma_bf16_ss(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb != kb0 || k != 0));
+            if constexpr (CG == 1)
+              umma_bf16_ss(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb != kb0 || k != 0));
+            else
+              umma_bf16_ss_2sm(d_tmem, a0 + 2 * k, b0 + 2 * k, idesc, (kb != kb0 || k != 0));
           }
-          tc_commit(&empty[s]);
+          if constexpr (CG == 1) tc_commit(&empty[s]);
+          else tc_commit_2sm_mc(&empty[s], 0x3);
         }
         __syncwarp();
         if (++s == STAGES) {
@@ -199,7 +248,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ph ^= 1;
         }
       }
-      if (lane == 0) tc_commit(&tfull[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) tc_commit(&tfull[acc]);
+        else tc_commit_2sm_mc(&tfull[acc], 0x3);
+      }
       __syncwarp();
     }
   } else if (warp >= 4) {
@@ -207,19 +259,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;  // TMEM lane quadrant
     const int row = q * 32 + lane;
     int it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
-      const int tile = u / splits;
-      const int split = u % splits;
+    // release an accumulator stage: one arrival per warp on the leader's barrier
+    auto release_acc = [&](int acc) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_cluster(&tempty[acc], 0);
+      }
+    };
+    for (int u = unit0; u < num_units; u += unit_step, ++it) {
+      int tile, split, splits, kb0, kb1;
+      unit_info(u, tile, split, splits, kb0, kb1);
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
-      const int m = mb * kGemmBM + row;
+      const int m = mb * Cfg::TILE_M + (int)rank * kGemmBM + row;
       const bool live = m < p.M;
       const int n0 = nb * BN;
       // Partial tiles are stored thread-major ([split][col/4][row] float4) so every warp
       // access is one contiguous 512-byte segment.
-      float4* ws_tile = reinterpret_cast<float4*>(p.ws) + (long long)tile * splits * (BN / 4) * kGemmBM;
+      const int wtile = (tile - full_tiles) * CG + (int)rank;  // workspace / ticket slot
+      float4* ws_tile =
+          reinterpret_cast<float4*>(p.ws) + (long long)wtile * splits * (BN / 4) * kGemmBM;
       const uint32_t tacc = tbase + acc * BN + ((uint32_t)(q * 32) << 16);
       if (splits > 1) {
         mbar_wait(&tfull[acc], acc_ph);
@@ -236,15 +299,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             st_global_v4(dst + (c * 8 + i) * kGemmBM,
                          make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]));
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        release_acc(acc);
         // 2) ticket: the last K-slice of the tile reduces and runs the epilogue
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (row == 0) {
-          const int old = atomicAdd(&p.tickets[tile], 1);
+          const int old = atomicAdd(&p.tickets[wtile], 1);
           s_last = old == splits - 1;
-          if (s_last) p.tickets[tile] = 0;
+          if (s_last) p.tickets[wtile] = 0;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (!s_last) continue;
@@ -408,18 +470,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
-      if (splits == 1) {
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-      }
+      if (splits == 1) release_acc(acc);
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/arrivals are all done
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<Cfg::TMEM_COLS>(tbase);
+    if constexpr (CG == 2) tmem_dealloc_2sm<Cfg::TMEM_COLS>(tbase);
+    else tmem_dealloc<Cfg::TMEM_COLS>(tbase);
   }
 }
 
