@@ -12,11 +12,14 @@ from collections import defaultdict
 
 
 def short(name):
-    m = re.search(r"(gemm_bf16_tn_kernel<(\d+), *(\d+)>|attn_prefill_tc_kernel|rmsnorm_kernel|init_normal_kernel|\w+)", name)
     epi = {"0": "store_bf16", "1": "store_f32(lm_head)", "2": "resid(o/down)", "3": "swiglu(gate_up)", "4": "qkv_rope_kv"}
-    if m and m.group(2):
-        return f"gemm BN={m.group(2)} {epi.get(m.group(3), m.group(3))}"
-    return m.group(1) if m else name[:40]
+    m = re.search(r"gemm_bf16_tn_kernel<(\d+), *(\d+), *(\d+)>", name)
+    if m:
+        return f"gemm {epi.get(m.group(2), m.group(2))} cta_group={m.group(3)}"
+    for k in ("attn_prefill_tc_kernel", "rmsnorm_kernel", "init_normal_kernel"):
+        if k in name:
+            return k
+    return name[:40]
 
 
 def launches(path):
