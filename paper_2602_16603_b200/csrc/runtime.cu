@@ -1040,11 +1040,14 @@ int fp_task_start(fp_ctx* c, fp_task* task, int32_t first) {
   Task* t = reinterpret_cast<Task*>(task);
   int rc = fp_task_begin_segment(c, task, first);
   if (rc) return rc;
-  {
+  for (int spin = 0;; ++spin) {  // a stopped segment's worker is still winding down
     std::lock_guard<std::mutex> lk(c->wmu);
-    if (c->wtask != nullptr) return set_err(FP_ERR_STATE, "pool occupied");
-    t->worker_active.store(1);
-    c->wtask = t;
+    if (c->wtask == nullptr) {
+      t->worker_active.store(1);
+      c->wtask = t;
+      break;
+    }
+    if (spin > 20000000) return set_err(FP_ERR_STATE, "pool occupied");
   }
   c->wcv.notify_all();
   return FP_OK;

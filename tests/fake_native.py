@@ -116,3 +116,76 @@ class FakeContext:
 
     def free_pages(self):
         return 0
+
+
+class FakeLiveTask:
+    """Wall-clock fake of an asynchronously running native task: each entry takes `entry_s`
+    seconds; a pending signal stops it at the next eligible boundary."""
+
+    def __init__(self, ctx, tokens, chunk, gran, task_id):
+        import time
+
+        self.ctx = ctx
+        self.time = time
+        lens = [len(t) for t in tokens]
+        n_chunks = len(F.plan(lens, chunk))
+        self.n_entries = n_chunks * ctx.num_layers * 5
+        self.gran = gran
+        self.task_id = task_id
+        self.state = 0
+        self.cursor = 0
+        self.seg_first = 0
+        self.t_start = None
+        self.starts = []
+        self.destroyed = False
+
+    def _eligible_after(self, i):
+        L = self.ctx.num_layers
+        op, layer = i % 5, (i // 5) % L
+        last = i == self.n_entries - 1
+        return {"operator": True, "layer": op == 4 or last,
+                "chunk": (op == 4 and layer == L - 1) or last}.get(self.gran, False)
+
+    def start(self, first):
+        assert self.state != RUNNING
+        self.seg_first = first
+        self.cursor = first
+        self.t_start = self.time.perf_counter()
+        self.state = RUNNING
+        self.starts.append(first)
+
+    def poll(self):
+        if self.state == RUNNING:
+            done = self.seg_first + int((self.time.perf_counter() - self.t_start) / self.ctx.entry_s)
+            while self.cursor < min(done, self.n_entries):
+                e = self.cursor
+                if e != self.seg_first and self.ctx.flag and self._eligible_after(e - 1):
+                    self.ctx.flag = 0
+                    self.state = STOPPED
+                    break
+                self.cursor += 1
+            if self.state == RUNNING and self.cursor >= self.n_entries:
+                self.state = DONE
+        return SimpleNamespace(state=self.state, cursor=self.cursor, generation=0)
+
+    def destroy(self):
+        self.destroyed = True
+
+
+class FakeLiveContext:
+    def __init__(self, num_layers=2, entry_s=50e-6):
+        self.num_layers = num_layers
+        self.entry_s = entry_s
+        self.flag = 0
+        self.tasks = []
+
+    def create_task(self, tokens, chunk, gran, task_id):
+        t = FakeLiveTask(self, tokens, chunk, gran, task_id)
+        self.tasks.append(t)
+        return t
+
+    def signal(self):
+        self.flag = 1
+
+    def clear(self):
+        self.flag = 0

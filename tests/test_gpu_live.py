@@ -1,0 +1,37 @@
+"""Wall-clock driver on the B200: reference scheduler + real asynchronous preemption."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_live_config1_trace(golden_dir):
+    from oracle import forward as F
+    from paper_2602_16603_b200 import refsim
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.engine import synthetic_tokens
+    from paper_2602_16603_b200.live import run_live
+    from paper_2602_16603_b200.native import PrefillContext
+
+    ps = refsim.load()
+    trace = ps.load_trace(os.path.join(golden_dir, "config1_trace.jsonl"))
+    trace = ps.scale_rate(trace, 10.0)  # 45 requests in ~2 s of wall time
+    shape = F.SHAPES["tiny"]
+    ctx = PrefillContext(SHAPES["tiny"], kv_pages=4096, max_pos=40000)
+    ctx.load_weights(F.make_weights(shape, 1234))
+    # cost model only weights progress() and the predictor; scaled to the tiny model on B200
+    params = ps.CostParams(num_layers=4)
+    res = run_live(trace, ps.PolicyConfig(), params, ctx, synthetic_tokens(1234, shape.vocab),
+                   record_events=True, max_wall_s=120)
+    assert sorted(o.id for o in res.outcomes) == sorted(r.id for r in trace.requests)
+    assert res.rounds == len(trace) + len(res.tasks)
+    assert res.commands["resume"] == res.commands["preempt"]
+    assert len(res.blocking_log) == res.commands["preempt"]
+    for sig, ack, _ in res.blocking_log:
+        assert ack - sig < 0.05
+    assert ctx.free_pages() == 4096
+    print("live:", res.commands, ps.slo_attainment(res.outcomes), ps.blocking_stats(res.blocking_log))
+    ctx.close()

@@ -1,0 +1,43 @@
+"""Wall-clock driver logic on CPU (fake asynchronous device): no lost requests, one round per
+arrival plus one per task completion (test_properties.py:80-84), every preemption is ACKed and
+resumed from the device cursor, blocking is bounded by one entry + polling slack."""
+
+import os
+
+import numpy as np
+import pytest
+
+from fake_native import FakeLiveContext
+
+
+@pytest.mark.parametrize("gran", ["operator", "layer"])
+def test_live_driver_invariants(gran):
+    from paper_2602_16603_b200 import refsim
+    from paper_2602_16603_b200.live import run_live
+
+    ps = refsim.load()
+    # a long request followed by urgent short ones, replayed in ~0.1 s of wall time
+    reqs = [ps.Request(0, "file", 0.0, 4000, 10.0)]
+    for i in range(1, 9):
+        reqs.append(ps.Request(i, "text", 0.005 * i, 50 + 7 * i, 0.05))
+    trace = ps.Trace(tuple(reqs))
+    params = ps.CostParams(num_layers=2)
+    ctx = FakeLiveContext(num_layers=2, entry_s=2e-3)
+    pc = ps.PolicyConfig(granularity=ps.PreemptionGranularity(gran))
+    res = run_live(trace, pc, params, ctx, tokens=lambda r: np.zeros(r.num_tokens, np.int32),
+                   record_events=True, max_wall_s=30)
+    assert sorted(o.id for o in res.outcomes) == list(range(9))
+    assert res.rounds == len(trace) + len(res.tasks)
+    assert res.commands["preempt"] >= 1
+    assert res.commands["resume"] == res.commands["preempt"]
+    assert len(res.blocking_log) == res.commands["preempt"]
+    for sig, ack, _ in res.blocking_log:
+        bound = 2e-3 * (5 if gran == "layer" else 1)
+        assert 0 <= ack - sig <= bound + 0.02
+    # every resume restarts exactly where the device stopped
+    acks = [e for e in res.events if e["kind"] == "preempt_ack"]
+    resumes = [e for e in res.events if e["kind"] == "resume"]
+    assert sorted(a["detail"]["cursor"] for a in acks) == sorted(r["detail"]["cursor"] for r in resumes)
+    for t in ctx.tasks:
+        assert t.destroyed
+    assert 0.0 <= ps.slo_attainment(res.outcomes) <= 1.0
