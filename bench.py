@@ -224,7 +224,8 @@ def run_ours(args):
     step_tokens = int(sum(lens))
     pages = sum((n + 127) // 128 for n in lens)
     long_len = 8192
-    ctx = PrefillContext(shape, device=device, kv_pages=2 * pages + long_len // 128 + 64,
+    live_pages = 0 if args.skip_live else 3000  # preempted tasks keep their KV pages
+    ctx = PrefillContext(shape, device=device, kv_pages=2 * pages + long_len // 128 + 64 + live_pages,
                          page_size=128, max_pos=40000)
     ctx.init_random(seed=0)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=device)
@@ -358,6 +359,16 @@ def run_ours(args):
         except Exception as e:  # keep the bench line even if the reference is unavailable
             good = {"error": repr(e)[:200]}
 
+    # -------- wall-clock check of the calibrated goodput: replay the config-2 trace in real time
+    if (rank == 0 and good is not None and "value" in good and not args.skip_live):
+        for t in tasks:
+            t.destroy()
+        tasks = []
+        try:
+            good["live_check"] = live_check(ctx, shape, good, args)
+        except Exception as e:
+            good["live_check"] = {"error": repr(e)[:300]}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:
         v, cores, sample = cpu_sample()
@@ -490,6 +501,42 @@ def preemption_latency(ctx, shape, rank: int, n_signals: int = 40, length: int =
     }
 
 
+def live_check(ctx, shape, good, args):
+    """Real-time replay (live driver) of the config-2 trace at the calibrated goodput rate:
+    S-EDF + operator preemption vs EDF + 2048-token chunked prefill (DistServe-CP analogue)."""
+    from paper_2602_16603_b200 import refsim
+    from paper_2602_16603_b200.live import run_live
+
+    ps = refsim.load()
+    params = ps.CostParams.from_json_dict(good["cost_params"])
+    rate = float(good["value"])
+    base = config2_trace(rate=20.0, duration=args.live_duration * rate / 20.0)
+    trace = ps.scale_rate(base, rate / base.base_rate())
+
+    def tok(r):
+        return np.random.default_rng(5000 + r.id).integers(0, shape.vocab, r.num_tokens).astype(np.int32)
+
+    out = {"rate_req_s": rate, "requests": len(trace),
+           "trace": f"config-2 trace, {args.live_duration:.0f} s of arrivals, seed 7"}
+    for name, pc in (("sedf_operator", ps.PolicyConfig()),
+                     ("edf_chunk2048", ps.PolicyConfig(policy=ps.PolicyKind.EDF,
+                                                       granularity=ps.PreemptionGranularity.CHUNK,
+                                                       chunk_tokens=2048))):
+        t0 = time.perf_counter()
+        res = run_live(trace, pc, params, ctx, tok, max_wall_s=10 * args.live_duration + 60)
+        bl = ps.blocking_stats(res.blocking_log)
+        out[name] = {
+            "attainment": ps.slo_attainment(res.outcomes),
+            "attainment_by_class": {c: ps.slo_attainment(res.outcomes, c)
+                                    for c in sorted({o.task for o in res.outcomes})},
+            "commands": res.commands,
+            "p99_blocking_ms": None if bl["p99_s"] is None else round(bl["p99_s"] * 1e3, 3),
+            "max_blocking_ms": None if bl["max_s"] is None else round(bl["max_s"] * 1e3, 3),
+            "wall_s": round(time.perf_counter() - t0, 2),
+        }
+    return out
+
+
 def calibrated_goodput(prof, shape, args):
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.calibrate import fit_cost_params, predicted_vs_measured
@@ -534,6 +581,8 @@ def main():
     ap.add_argument("--skip-goodput", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--goodput-duration", type=float, default=60.0)
+    ap.add_argument("--skip-live", action="store_true")
+    ap.add_argument("--live-duration", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -35,3 +35,34 @@ def test_live_config1_trace(golden_dir):
     assert ctx.free_pages() == 4096
     print("live:", res.commands, ps.slo_attainment(res.outcomes), ps.blocking_stats(res.blocking_log))
     ctx.close()
+
+
+def test_live_preemption_llama_shape():
+    """Llama-3-8B layer shapes (4 layers): a 16K-token request is preempted by urgent short
+    requests; every ACK lands within about one operator of the signal."""
+    from dataclasses import replace
+
+    from paper_2602_16603_b200 import refsim
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.engine import synthetic_tokens
+    from paper_2602_16603_b200.live import run_live
+    from paper_2602_16603_b200.native import PrefillContext
+
+    ps = refsim.load()
+    shape = replace(SHAPES["llama3-8b"], num_layers=4)
+    ctx = PrefillContext(shape, kv_pages=256, max_pos=40000)
+    ctx.init_random(0)
+    reqs = [ps.Request(0, "file", 0.0, 16384, 10.0)]
+    for i in range(1, 6):
+        reqs.append(ps.Request(i, "text", 0.004 * i, 300 + 50 * i, 0.05))
+    trace = ps.Trace(tuple(reqs))
+    params = ps.CostParams(num_layers=4)
+    res = run_live(trace, ps.PolicyConfig(), params, ctx, synthetic_tokens(0, shape.vocab),
+                   record_events=True, max_wall_s=120)
+    assert sorted(o.id for o in res.outcomes) == list(range(6))
+    assert res.commands["preempt"] >= 1
+    assert res.commands["resume"] == res.commands["preempt"]
+    bl = ps.blocking_stats(res.blocking_log)
+    print("live llama4L:", res.commands, ps.slo_attainment(res.outcomes), bl)
+    assert bl["max_s"] < 0.02  # one operator at 16K tokens is a few ms on a B200
+    ctx.close()
