@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // residual row segment prefetched into registers while the MMA runs
         uint4 hres[BN / 8];
         __nv_bfloat16* hrow = p.resid + (long long)m * p.ldr + n0;
-        if (live) {
+        if (live && splits == 1) {
 #pragma unroll
           for (int i = 0; i < BN / 8; ++i) hres[i] = ld_global_v4(hrow + 8 * i);
         }
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (live) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const uint4 h = hres[c * 4 + i];
+              const uint4 h = splits == 1 ? hres[c * 4 + i] : ld_global_v4(hrow + c * 32 + 8 * i);
               const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {

@@ -170,6 +170,8 @@ struct fp_ctx {
   float* ws = nullptr;
   int* tickets = nullptr;
   bool use_pair_gemm = true;
+  int force_splits = 0;   // FP_FORCE_SPLITS (experiments)
+  int force_pair = -1;    // FP_FORCE_PAIR (experiments): 0 single, 1 pair
 };
 
 static cudaEvent_t ev_get(fp_ctx* c) {
@@ -239,7 +241,13 @@ static double choose_splits(int tiles, int num_k, int num_sms, int* full_tiles, 
   const double full_cost = (double)(tiles / num_sms) * (num_k + 4.0);
   *full_tiles = tiles - rem;
   *splits = 1;
-  if (rem == 0) return full_cost;
+  // Measured on B200 (tools/split_sweep.py): a K-slice costs ~15 us of partial traffic and
+  // reduction regardless of its length, so splitting only pays for long-K GEMMs (down_proj,
+  // K = 14336) whose remainder is under half a wave.
+  if (rem == 0 || num_k < 128 || rem * 2 > num_sms) {
+    if (rem) *full_tiles = tiles;
+    return full_cost + (rem ? num_k + 4.0 : 0.0);
+  }
   double best_t = 1e30;
   for (int S = 1; S <= 8; ++S) {
     if (S > 1 && (num_k / S < 4 || rem * S > 2 * num_sms)) break;
@@ -272,6 +280,12 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   p.full_tiles = tiles;
   if (c->ws && EPI != EPI_STORE_F32)
     choose_splits(tiles, p.K / kGemmBK, slots, &p.full_tiles, &p.splits);
+  if (c->force_splits > 0) {  // experiments only (FP_FORCE_SPLITS)
+    const int rem = tiles % slots;
+    p.splits = c->force_splits;
+    p.full_tiles = (p.splits > 1 && rem) ? tiles - rem : tiles;
+    if (p.splits > 1 && rem == 0) p.full_tiles = tiles;
+  }
   p.ws = c->ws;
   p.tickets = c->tickets;
   const int units = p.full_tiles + (tiles - p.full_tiles) * p.splits;
@@ -298,6 +312,7 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
 // B200: less shared-memory traffic per k-block) but pad M to 256 rows and halve the number
 // of concurrent tiles. Shape-only decision.
 static bool pick_pair(const fp_ctx* c, int M, int N, int K) {
+  if (c->force_pair >= 0) return c->force_pair == 1 && M > kGemmBM;
   if (!c->use_pair_gemm || M <= kGemmBM) return false;
   int ft, sp;
   const int nN = N / 256, num_k = K / kGemmBK;
@@ -606,6 +621,8 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   CK(cudaMemset(c->kv, 0, (size_t)L * kv_pages * c->page_elems * 2));
   {
     if (const char* e = getenv("FP_PAIR_GEMM")) c->use_pair_gemm = atoi(e) != 0;
+    if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
+    if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
     const uint64_t rows = (uint64_t)L * kv_pages * 2 * cfg->n_kv_heads * page_size;
     REQ(rows < (1ull << 31), "KV pool too large for 32-bit TMA row coordinates");
     int rc = make_map(&c->tm_kv, c->kv, rows, 128, 128);
@@ -613,7 +630,7 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   }
   c->free_pages.resize(kv_pages);
   for (long long i = 0; i < kv_pages; ++i) c->free_pages[i] = (int)(kv_pages - 1 - i);
-  CK(cudaMalloc(&c->ws, (size_t)2 * c->num_sms * kGemmBM * 256 * sizeof(float)));
+  CK(cudaMalloc(&c->ws, (size_t)8 * c->num_sms * kGemmBM * 256 * sizeof(float)));
   CK(cudaMalloc(&c->tickets, 4096 * sizeof(int)));
   CK(cudaMemset(c->tickets, 0, 4096 * sizeof(int)));
   CK(cudaHostAlloc(&c->hctl, sizeof(HostCtl), cudaHostAllocMapped));

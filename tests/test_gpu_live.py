@@ -52,9 +52,14 @@ def test_live_preemption_llama_shape():
     shape = replace(SHAPES["llama3-8b"], num_layers=4)
     ctx = PrefillContext(shape, kv_pages=256, max_pos=40000)
     ctx.init_random(0)
+    warm = ctx.create_task([np.zeros(16384, np.int32)])  # first-use costs off the clock
+    warm.begin_segment(0)
+    warm.enqueue(0, warm.n_entries)
+    ctx.sync()
+    warm.destroy()
     reqs = [ps.Request(0, "file", 0.0, 16384, 10.0)]
     for i in range(1, 6):
-        reqs.append(ps.Request(i, "text", 0.004 * i, 300 + 50 * i, 0.05))
+        reqs.append(ps.Request(i, "text", 0.006 * i, 300 + 50 * i, 0.3))
     trace = ps.Trace(tuple(reqs))
     params = ps.CostParams(num_layers=4)
     res = run_live(trace, ps.PolicyConfig(), params, ctx, synthetic_tokens(0, shape.vocab),
