@@ -53,6 +53,11 @@ extern "C" {
 #define FP_W_FFN_NORM 9   /* [hidden] */
 #define FP_W_FINAL_NORM 10 /* [hidden] */
 #define FP_W_LM_HEAD 11   /* [vocab, hidden] */
+#define FP_W_Q_BIAS 12    /* [n_heads*head_dim]      (Qwen2.5: qkv_bias) */
+#define FP_W_K_BIAS 13    /* [n_kv_heads*head_dim] */
+#define FP_W_V_BIAS 14    /* [n_kv_heads*head_dim] */
+#define FP_W_Q_NORM 15    /* [head_dim]              (Qwen3: qk_norm) */
+#define FP_W_K_NORM 16    /* [head_dim] */
 
 typedef struct fp_model_cfg {
   int32_t num_layers; /* CostParams.num_layers, cost_model.py:92 */
@@ -61,10 +66,12 @@ typedef struct fp_model_cfg {
   int32_t n_kv_heads;
   int32_t head_dim; /* must be 128 */
   int32_t ffn;
-  int32_t vocab;
+  int32_t vocab;   /* any size; padded internally to a multiple of 256 */
   int32_t max_pos; /* RoPE table length */
   float rope_theta;
   float rms_eps;
+  int32_t qkv_bias; /* 1: q/k/v projections carry a bias (Qwen2.5) */
+  int32_t qk_norm;  /* 1: per-head RMSNorm of q and k before RoPE (Qwen3) */
 } fp_model_cfg;
 
 typedef struct fp_ctx fp_ctx;

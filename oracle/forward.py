@@ -52,6 +52,8 @@ class Shape:
     vocab: int
     rope_theta: float
     rms_eps: float = 1e-5
+    qkv_bias: bool = False  # Qwen2.5: biases on q/k/v projections
+    qk_norm: bool = False   # Qwen3: per-head RMSNorm of q and k before RoPE
 
     @property
     def qdim(self) -> int:
@@ -67,6 +69,9 @@ SHAPES = {
     "tiny": Shape(4, 512, 4, 2, 128, 1536, 8192, 1e4),
     # configs[1]: Llama-3-8B shape (public model card values)
     "llama3-8b": Shape(32, 4096, 32, 8, 128, 14336, 128256, 5e5),
+    # small Qwen-style variants for parity tests (vocab not a multiple of 256 on purpose)
+    "tiny-qwen3": Shape(2, 512, 4, 2, 128, 1536, 8000, 1e6, 1e-6, qk_norm=True),
+    "tiny-qwen2": Shape(2, 512, 4, 2, 128, 1536, 8000, 1e6, 1e-6, qkv_bias=True),
 }
 
 
@@ -106,6 +111,13 @@ def make_weights(shape: Shape, seed: int, std: float = 0.02) -> dict:
         w[f"{l}.w_down"] = normal(d, f)
         w[f"{l}.attn_norm"] = gamma(d)
         w[f"{l}.ffn_norm"] = gamma(d)
+        if shape.qkv_bias:
+            w[f"{l}.bq"] = normal(shape.qdim) * 10.0
+            w[f"{l}.bk"] = normal(shape.kvdim) * 10.0
+            w[f"{l}.bv"] = normal(shape.kvdim) * 10.0
+        if shape.qk_norm:
+            w[f"{l}.q_norm"] = gamma(shape.head_dim)
+            w[f"{l}.k_norm"] = gamma(shape.head_dim)
     w["final_norm"] = gamma(d)
     w["lm_head"] = normal(shape.vocab, d)
     return w
@@ -293,9 +305,15 @@ class OracleTask:
                 self.h = w["embed"][self.stream[ch.start : ch.end]].astype(np.float32)
             xn = rmsnorm(self.h, w[P + "attn_norm"], sh.rms_eps)
             n = ch.new_total
-            q = (xn @ w[P + "wq"].T).reshape(n, sh.n_heads, sh.head_dim)
-            k = (xn @ w[P + "wk"].T).reshape(n, sh.n_kv_heads, sh.head_dim)
-            v = (xn @ w[P + "wv"].T).reshape(n, sh.n_kv_heads, sh.head_dim)
+            q, k, v = xn @ w[P + "wq"].T, xn @ w[P + "wk"].T, xn @ w[P + "wv"].T
+            if sh.qkv_bias:
+                q, k, v = q + w[P + "bq"], k + w[P + "bk"], v + w[P + "bv"]
+            q = q.reshape(n, sh.n_heads, sh.head_dim)
+            k = k.reshape(n, sh.n_kv_heads, sh.head_dim)
+            v = v.reshape(n, sh.n_kv_heads, sh.head_dim)
+            if sh.qk_norm:
+                q = rmsnorm(q, w[P + "q_norm"], sh.rms_eps)
+                k = rmsnorm(k, w[P + "k_norm"], sh.rms_eps)
             cos, sin = rope_tables(self._positions(ch), sh.head_dim, sh.rope_theta)
             self.q = apply_rope(q, cos, sin)
             k = apply_rope(k, cos, sin)

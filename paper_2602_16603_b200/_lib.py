@@ -20,6 +20,7 @@ FP_TASK_IDLE, FP_TASK_RUNNING, FP_TASK_STOPPED, FP_TASK_DONE = 0, 1, 2, 3
 
 W_EMBED, W_Q, W_K, W_V, W_O, W_GATE, W_UP, W_DOWN = range(8)
 W_ATTN_NORM, W_FFN_NORM, W_FINAL_NORM, W_LM_HEAD = 8, 9, 10, 11
+W_Q_BIAS, W_K_BIAS, W_V_BIAS, W_Q_NORM, W_K_NORM = 12, 13, 14, 15, 16
 
 
 class NativeError(RuntimeError):
@@ -38,6 +39,8 @@ class ModelCfg(C.Structure):
         ("max_pos", C.c_int32),
         ("rope_theta", C.c_float),
         ("rms_eps", C.c_float),
+        ("qkv_bias", C.c_int32),
+        ("qk_norm", C.c_int32),
     ]
 
 

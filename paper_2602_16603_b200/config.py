@@ -17,6 +17,8 @@ class ModelShape:
     vocab: int
     rope_theta: float
     rms_eps: float = 1e-5
+    qkv_bias: bool = False  # Qwen2.5
+    qk_norm: bool = False   # Qwen3
 
     @property
     def qdim(self) -> int:
@@ -44,8 +46,15 @@ class ModelShape:
 SHAPES = {
     "tiny": ModelShape("tiny", 4, 512, 4, 2, 128, 1536, 8192, 1e4),
     "llama3-8b": ModelShape("llama3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 5e5),
-    # configs[2] (independent instances); q/k-norm not modelled in this build
-    "qwen3-8b": ModelShape("qwen3-8b", 36, 4096, 32, 8, 128, 12288, 151936, 1e6, 1e-6),
-    # configs[3] (TP); QKV bias not modelled in this build
-    "qwen2.5-32b": ModelShape("qwen2.5-32b", 64, 5120, 40, 8, 128, 27648, 152064, 1e6, 1e-6),
+    # configs[2]: independent per-GPU instances
+    "qwen3-8b": ModelShape("qwen3-8b", 36, 4096, 32, 8, 128, 12288, 151936, 1e6, 1e-6,
+                           qk_norm=True),
+    # configs[3]: tensor parallel
+    "qwen2.5-32b": ModelShape("qwen2.5-32b", 64, 5120, 40, 8, 128, 27648, 152064, 1e6, 1e-6,
+                              qkv_bias=True),
+    # parity-test variants (match oracle.forward.SHAPES)
+    "tiny-qwen3": ModelShape("tiny-qwen3", 2, 512, 4, 2, 128, 1536, 8000, 1e6, 1e-6,
+                             qk_norm=True),
+    "tiny-qwen2": ModelShape("tiny-qwen2", 2, 512, 4, 2, 128, 1536, 8000, 1e6, 1e-6,
+                             qkv_bias=True),
 }

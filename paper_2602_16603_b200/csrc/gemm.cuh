@@ -42,6 +42,11 @@ struct GemmParams {
   __nv_bfloat16* kv_layer;  // this layer's base of the paged KV pool
   const float2* rope;       // [max_pos][64] (cos, sin)
   int q_cols, kv_cols, page_size, n_kv_heads;
+  const float* bias;        // [N] q/k/v projection bias (Qwen2.5) or null
+  const float* q_norm;      // [128] per-head RMSNorm weight of q (Qwen3) or null
+  const float* k_norm;      // [128] ... of k
+  float norm_eps;
+  int pad2;
   // Tail split-K: the first `full_tiles` tiles (whole waves) run unsplit; each remaining tile
   // is cut into `splits` K-slices so the last wave fills the machine. fp32 partials go to
   // `ws` and the last-arriving CTA of a tile reduces them in split order (deterministic) and
@@ -445,6 +450,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                    (pos % p.page_size)) *
                       128;
           }
+          const float* bias = p.bias ? p.bias + col0 : nullptr;
+          const float* hn = is_v ? nullptr : (is_q ? p.q_norm : p.k_norm);
+          float nscale = 1.f;
+          if (hn != nullptr) {  // per-head RMSNorm (Qwen3): sum of squares over the head first
+            float ss = 0.f;
+#pragma unroll 1
+            for (int c4 = 0; c4 < 4; ++c4) {
+              float a[32];
+              load32(hh * 128 + c4 * 32, a);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float x = a[i] + (bias ? __ldg(bias + c4 * 32 + i) : 0.f);
+                ss += x * x;
+              }
+            }
+            nscale = rsqrtf(ss * (1.f / 128.f) + p.norm_eps);
+          }
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             // chunk pair (half, half+2): columns j and j+64 of the head for j in this chunk
@@ -452,6 +474,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             load32(hh * 128 + half * 32, a);
             load32(hh * 128 + half * 32 + 64, b);
             if (live) {
+              if (bias) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  a[i] += __ldg(bias + half * 32 + i);
+                  b[i] += __ldg(bias + half * 32 + 64 + i);
+                }
+              }
+              if (hn) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  a[i] *= nscale * __ldg(hn + half * 32 + i);
+                  b[i] *= nscale * __ldg(hn + half * 32 + 64 + i);
+                }
+              }
               if (!is_v) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {

@@ -96,6 +96,8 @@ __global__ void init_normal_kernel(__nv_bfloat16* w, long long n, uint64_t seed,
 // --------------------------------------------------------------------------- structures
 struct Layer {
   __nv_bfloat16 *wqkv, *wo, *wgu, *wd, *attn_g, *ffn_g;
+  float* bqkv = nullptr;                           // [qkv_n] (qkv_bias models)
+  float *q_norm = nullptr, *k_norm = nullptr;      // [128]  (qk_norm models)
   CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
 };
 
@@ -132,7 +134,7 @@ struct Task {
 struct fp_ctx {
   int device = 0, num_sms = 148;
   fp_model_cfg cfg{};
-  int qdim = 0, kvdim = 0, qkv_n = 0;
+  int qdim = 0, kvdim = 0, qkv_n = 0, vocab_pad = 0;
   cudaStream_t stream = nullptr, upload = nullptr;
   std::vector<Layer> layers;
   __nv_bfloat16 *embed = nullptr, *final_g = nullptr, *lm_head = nullptr;
@@ -426,6 +428,10 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
       p.kv_cols = c->kvdim;
       p.page_size = c->page_size;
       p.n_kv_heads = m.n_kv_heads;
+      p.bias = ly.bqkv;
+      p.q_norm = ly.q_norm;
+      p.k_norm = ly.k_norm;
+      p.norm_eps = m.rms_eps;
       ProfScope ps(c, st, FP_K_QKV, layer, M, 2.0 * M * p.N * p.K, 0.0);
       launch_gemm<EPI_QKV>(c, t->tm_xn, ly.tm_qkv, p, st);
     } else {
@@ -490,10 +496,10 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
         }
         GemmParams q{};
         q.M = ch.n_last;
-        q.N = m.vocab;
+        q.N = c->vocab_pad;
         q.K = m.hidden;
-        q.out = t->logits + (long long)ch.seq0 * m.vocab;
-        q.ldo = m.vocab;
+        q.out = t->logits + (long long)ch.seq0 * c->vocab_pad;
+        q.ldo = c->vocab_pad;
         q.guard = g2;
         ProfScope ps(c, st, FP_K_LM_HEAD, layer, ch.n_last, 2.0 * ch.n_last * q.N * q.K, 0.0);
         launch_gemm<EPI_STORE_F32>(c, t->tm_xf, c->tm_lm, q, st);
@@ -555,7 +561,6 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   REQ(cfg->hidden % 256 == 0 && cfg->ffn % 128 == 0, "hidden%256 and ffn%128 required");
   REQ(cfg->n_heads % cfg->n_kv_heads == 0, "n_heads must be a multiple of n_kv_heads");
   REQ(((cfg->n_heads + 2 * cfg->n_kv_heads) * 128) % 256 == 0, "qkv width must be %256");
-  REQ(cfg->vocab % 256 == 0, "vocab must be a multiple of 256");
   REQ(page_size == 128, "page_size must be 128 (one attention KV tile per page)");
   REQ(kv_pages > 0, "kv_pages must be > 0");
   CK(cudaSetDevice(device));
@@ -590,6 +595,14 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     CK(cudaMalloc(&ly.wd, (size_t)d * cfg->ffn * 2));
     CK(cudaMalloc(&ly.attn_g, (size_t)d * 2));
     CK(cudaMalloc(&ly.ffn_g, (size_t)d * 2));
+    if (cfg->qkv_bias) {
+      CK(cudaMalloc(&ly.bqkv, (size_t)c->qkv_n * 4));
+      CK(cudaMemset(ly.bqkv, 0, (size_t)c->qkv_n * 4));
+    }
+    if (cfg->qk_norm) {
+      CK(cudaMalloc(&ly.q_norm, 128 * 4));
+      CK(cudaMalloc(&ly.k_norm, 128 * 4));
+    }
     int rc;
     if ((rc = make_map(&ly.tm_qkv, ly.wqkv, c->qkv_n, d, 128))) return rc;
     if ((rc = make_map(&ly.tm_o, ly.wo, d, c->qdim, 128))) return rc;
@@ -597,10 +610,12 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     if ((rc = make_map(&ly.tm_d, ly.wd, d, cfg->ffn, 128))) return rc;
   }
   CK(cudaMalloc(&c->embed, (size_t)cfg->vocab * d * 2));
-  CK(cudaMalloc(&c->lm_head, (size_t)cfg->vocab * d * 2));
+  c->vocab_pad = (cfg->vocab + 255) / 256 * 256;  // lm_head GEMM tiles are 256 wide
+  CK(cudaMalloc(&c->lm_head, (size_t)c->vocab_pad * d * 2));
+  CK(cudaMemset(c->lm_head, 0, (size_t)c->vocab_pad * d * 2));
   CK(cudaMalloc(&c->final_g, (size_t)d * 2));
   {
-    int rc = make_map(&c->tm_lm, c->lm_head, cfg->vocab, d, 128);
+    int rc = make_map(&c->tm_lm, c->lm_head, c->vocab_pad, d, 128);
     if (rc) return rc;
   }
   // RoPE table (rotate-half convention), fp64 on the host
@@ -659,6 +674,9 @@ int fp_ctx_destroy(fp_ctx* c) {
     cudaFree(ly.wd);
     cudaFree(ly.attn_g);
     cudaFree(ly.ffn_g);
+    cudaFree(ly.bqkv);
+    cudaFree(ly.q_norm);
+    cudaFree(ly.k_norm);
   }
   cudaFree(c->embed);
   cudaFree(c->lm_head);
@@ -726,9 +744,34 @@ static __nv_bfloat16* weight_ptr(fp_ctx* c, int tensor, int layer, long long* n_
   return nullptr;
 }
 
+// bf16 host vector -> fp32 device vector (biases, q/k norm weights live in fp32)
+static int load_f32_vec(float* dst, const void* host, int64_t n) {
+  std::vector<float> f(n);
+  const uint16_t* h = static_cast<const uint16_t*>(host);
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u = (uint32_t)h[i] << 16;
+    memcpy(&f[i], &u, 4);
+  }
+  CK(cudaMemcpy(dst, f.data(), n * 4, cudaMemcpyHostToDevice));
+  return FP_OK;
+}
+
 int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, int64_t n) {
   REQ(c && host, "null argument");
   CK(cudaSetDevice(c->device));
+  if (tensor >= FP_W_Q_BIAS && tensor <= FP_W_K_NORM) {
+    REQ(layer >= 0 && layer < c->cfg.num_layers, "bad layer");
+    Layer& ly = c->layers[layer];
+    if (tensor <= FP_W_V_BIAS) {
+      REQ(ly.bqkv != nullptr, "model has no qkv bias");
+      const long long off = tensor == FP_W_Q_BIAS ? 0 : (tensor == FP_W_K_BIAS ? c->qdim : c->qdim + c->kvdim);
+      REQ(n == (tensor == FP_W_Q_BIAS ? c->qdim : c->kvdim), "bias size mismatch");
+      return load_f32_vec(ly.bqkv + off, host, n);
+    }
+    REQ(ly.q_norm != nullptr, "model has no q/k norm");
+    REQ(n == 128, "q/k norm size must be head_dim");
+    return load_f32_vec(tensor == FP_W_Q_NORM ? ly.q_norm : ly.k_norm, host, n);
+  }
   long long need = 0, off = 0;
   __nv_bfloat16* dst = weight_ptr(c, tensor, layer, &need, &off);
   REQ(dst != nullptr, "unknown tensor/layer");
@@ -768,6 +811,15 @@ int fp_weights_init_random(fp_ctx* c, uint64_t seed, float stdv) {
     fill(ly.wd, d * m.ffn, 0.f, stdv);
     fill(ly.attn_g, d, 1.f, 0.1f);
     fill(ly.ffn_g, d, 1.f, 0.1f);
+    if (ly.bqkv || ly.q_norm) {
+      std::vector<float> v(c->qkv_n);
+      for (int i = 0; i < c->qkv_n; ++i) v[i] = 0.02f * (float)((int)((s * 2654435761ull + i * 40503ull) % 2001) - 1000) / 1000.f;
+      if (ly.bqkv) CK(cudaMemcpy(ly.bqkv, v.data(), c->qkv_n * 4, cudaMemcpyHostToDevice));
+      for (int i = 0; i < 128; ++i) v[i] = 1.f + 5.f * v[i];
+      if (ly.q_norm) CK(cudaMemcpy(ly.q_norm, v.data(), 512, cudaMemcpyHostToDevice));
+      if (ly.k_norm) CK(cudaMemcpy(ly.k_norm, v.data(), 512, cudaMemcpyHostToDevice));
+      ++s;
+    }
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
@@ -935,8 +987,8 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   CK(cudaMallocAsync((void**)&t->ao, M * c->qdim * 2, up));
   CK(cudaMallocAsync((void**)&t->act, M * (long long)m.ffn * 2, up));
   CK(cudaMallocAsync((void**)&t->xf, (long long)n_seqs * d * 2, up));
-  CK(cudaMallocAsync((void**)&t->logits, (long long)n_seqs * m.vocab * 4, up));
-  CK(cudaMemsetAsync(t->logits, 0, (long long)n_seqs * m.vocab * 4, up));
+  CK(cudaMallocAsync((void**)&t->logits, (long long)n_seqs * c->vocab_pad * 4, up));
+  CK(cudaMemsetAsync(t->logits, 0, (long long)n_seqs * c->vocab_pad * 4, up));
   const size_t ctl_bytes = sizeof(TaskCtl) + (size_t)t->n_entries * 4;
   CK(cudaMallocAsync((void**)&t->ctl, ctl_bytes, up));
   CK(cudaMemsetAsync(t->ctl, 0, ctl_bytes, up));
@@ -1129,8 +1181,8 @@ int fp_task_logits(fp_ctx* c, fp_task* task, float* host_out) {
   REQ(c && t && host_out, "null argument");
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
-  CK(cudaMemcpy(host_out, t->logits, (size_t)t->n_seqs * c->cfg.vocab * 4,
-                cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy2D(host_out, (size_t)c->cfg.vocab * 4, t->logits, (size_t)c->vocab_pad * 4,
+                  (size_t)c->cfg.vocab * 4, t->n_seqs, cudaMemcpyDeviceToHost));
   return FP_OK;
 }
 

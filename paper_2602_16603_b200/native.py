@@ -42,6 +42,11 @@ _WEIGHT_IDS = {
     "w_down": _lib.W_DOWN,
     "attn_norm": _lib.W_ATTN_NORM,
     "ffn_norm": _lib.W_FFN_NORM,
+    "bq": _lib.W_Q_BIAS,
+    "bk": _lib.W_K_BIAS,
+    "bv": _lib.W_V_BIAS,
+    "q_norm": _lib.W_Q_NORM,
+    "k_norm": _lib.W_K_NORM,
 }
 
 
@@ -71,6 +76,8 @@ class PrefillContext:
             max_pos,
             shape.rope_theta,
             shape.rms_eps,
+            int(shape.qkv_bias),
+            int(shape.qk_norm),
         )
         h = C.c_void_p()
         _lib.check(
@@ -103,7 +110,8 @@ class PrefillContext:
         put(_lib.W_FINAL_NORM, -1, w["final_norm"])
         for l in range(self.shape.num_layers):
             for name, tid in _WEIGHT_IDS.items():
-                put(tid, l, w[f"{l}.{name}"])
+                if f"{l}.{name}" in w:
+                    put(tid, l, w[f"{l}.{name}"])
 
     # -- tasks -----------------------------------------------------------------------
     def create_task(

@@ -71,6 +71,52 @@ def hf_logits(shape: F.Shape, w: dict, tokens: list) -> np.ndarray:
     return np.stack(out).astype(np.float32)
 
 
+def hf_qwen_logits(shape: F.Shape, w: dict, tokens: list) -> np.ndarray:
+    import torch
+
+    if shape.qk_norm:
+        from transformers import Qwen3Config as Cfg, Qwen3ForCausalLM as Model
+    else:
+        from transformers import Qwen2Config as Cfg, Qwen2ForCausalLM as Model
+    kw = dict(vocab_size=shape.vocab, hidden_size=shape.hidden, intermediate_size=shape.ffn,
+              num_hidden_layers=shape.num_layers, num_attention_heads=shape.n_heads,
+              num_key_value_heads=shape.n_kv_heads, rope_theta=shape.rope_theta,
+              rms_norm_eps=shape.rms_eps, tie_word_embeddings=False,
+              max_position_embeddings=65536, attn_implementation="eager")
+    if shape.qk_norm:
+        kw["head_dim"] = shape.head_dim
+    model = Model(Cfg(**kw)).float().eval()
+    sd = {"model.embed_tokens.weight": w["embed"], "lm_head.weight": w["lm_head"],
+          "model.norm.weight": w["final_norm"]}
+    for l in range(shape.num_layers):
+        p = f"model.layers.{l}."
+        for hf, ours in (("self_attn.q_proj.weight", "wq"), ("self_attn.k_proj.weight", "wk"),
+                         ("self_attn.v_proj.weight", "wv"), ("self_attn.o_proj.weight", "wo"),
+                         ("mlp.gate_proj.weight", "w_gate"), ("mlp.up_proj.weight", "w_up"),
+                         ("mlp.down_proj.weight", "w_down"),
+                         ("input_layernorm.weight", "attn_norm"),
+                         ("post_attention_layernorm.weight", "ffn_norm")):
+            sd[p + hf] = w[f"{l}.{ours}"]
+        if shape.qkv_bias:
+            sd[p + "self_attn.q_proj.bias"] = w[f"{l}.bq"]
+            sd[p + "self_attn.k_proj.bias"] = w[f"{l}.bk"]
+            sd[p + "self_attn.v_proj.bias"] = w[f"{l}.bv"]
+        if shape.qk_norm:
+            sd[p + "self_attn.q_norm.weight"] = w[f"{l}.q_norm"]
+            sd[p + "self_attn.k_norm.weight"] = w[f"{l}.k_norm"]
+    missing = set(model.state_dict()) - set(sd)
+    missing = {m for m in missing if "rotary" not in m}
+    assert not missing, missing
+    model.load_state_dict({k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in sd.items()},
+                          strict=False)
+    out = []
+    with torch.no_grad():
+        for t in tokens:
+            ids = torch.from_numpy(t.astype(np.int64))[None]
+            out.append(model(input_ids=ids).logits[0, -1].numpy())
+    return np.stack(out).astype(np.float32)
+
+
 def reference_events() -> None:
     for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
         if os.path.isdir(os.path.join(p, "prefillsim")):
@@ -106,6 +152,17 @@ def main() -> None:
     assert err < 1e-3, err
     np.savez_compressed(os.path.join(HERE, "tiny_hf_logits.npz"), seed=TINY_SEED,
                         lens=np.array(TINY_LENS), logits=ref)
+    for name in ("tiny-qwen3", "tiny-qwen2"):
+        sh = F.SHAPES[name]
+        wq = F.make_weights(sh, TINY_SEED)
+        toks = F.make_tokens(TINY_LENS, sh.vocab, TINY_SEED)
+        ref = hf_qwen_logits(sh, wq, toks)
+        ours = F.forward_logits(sh, wq, toks)
+        err = np.abs(ours - ref).max()
+        print(f"oracle vs HF {name}: max abs err", err, "max |logit|", np.abs(ref).max())
+        assert err < 1e-3, err
+        np.savez_compressed(os.path.join(HERE, f"{name}_hf_logits.npz"), seed=TINY_SEED,
+                            lens=np.array(TINY_LENS), logits=ref)
     reference_events()
 
 

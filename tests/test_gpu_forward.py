@@ -136,3 +136,32 @@ def test_preemption_bitwise_and_cursor(tiny, gran):
     assert t.poll().state == 3
     assert np.array_equal(t.logits(), lref)
     t.destroy()
+
+
+@pytest.mark.parametrize("name", ["tiny-qwen3", "tiny-qwen2"])
+def test_qwen_variants_vs_hf_and_oracle(golden_dir, name):
+    """Qwen3 q/k-norm and Qwen2.5 QKV bias in the fused QKV epilogue; vocab 8000 (not a
+    multiple of 256: lm_head padded internally)."""
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    shape = F.SHAPES[name]
+    w = F.make_weights(shape, 1234)
+    ctx = PrefillContext(SHAPES[name], kv_pages=64, max_pos=4096)
+    ctx.load_weights(w)
+    g = np.load(f"{golden_dir}/{name}_hf_logits.npz")
+    tokens = F.make_tokens(list(g["lens"]), shape.vocab, int(g["seed"]))
+    t = run_straight(ctx, tokens, 96)
+    lg = t.logits()
+    assert lg.shape == (len(tokens), 8000)
+    e = rel_err(lg, g["logits"])
+    print(f"{name} GPU vs HF: {e:.4g}")
+    assert e <= LOGIT_ATOL_FRAC
+    ot = F.OracleTask(shape, w, tokens, 96)
+    ot.run_all()
+    for r in range(len(tokens)):
+        k, v = t.read_kv(r, 1)
+        assert rel_err(k, ot.k_cache[r][1]) <= KV_ATOL_FRAC
+        assert rel_err(v, ot.v_cache[r][1]) <= KV_ATOL_FRAC
+    t.destroy()
+    ctx.close()

@@ -94,3 +94,13 @@ def test_reference_goldens_reproduce(ps, golden_dir):
     lines = "".join(json.dumps(ev, sort_keys=True) + "\n" for ev in res.events)
     assert lines == open(os.path.join(golden_dir, "config1_events.jsonl")).read()
     assert res.commands == {"submit": 45, "preempt": 2, "resume": 2}
+
+
+@pytest.mark.parametrize("name", ["tiny-qwen3", "tiny-qwen2"])
+def test_oracle_matches_hf_qwen_goldens(golden_dir, name):
+    """q/k-norm (Qwen3) and QKV bias (Qwen2.5) variants pinned to HF Qwen3/Qwen2 models."""
+    g = np.load(os.path.join(golden_dir, f"{name}_hf_logits.npz"))
+    shape = F.SHAPES[name]
+    w = F.make_weights(shape, int(g["seed"]))
+    tokens = F.make_tokens(list(g["lens"]), shape.vocab, int(g["seed"]))
+    np.testing.assert_allclose(F.forward_logits(shape, w, tokens), g["logits"], rtol=0, atol=1e-4)
