@@ -104,7 +104,13 @@ const char* fp_last_error(void);
 int fp_version(void);
 
 /* ---- context (one execution pool per device) ---------------------------------------- */
-/* Replaces Engine.__init__ (engine.py:161-179). tp_size must be 1 in this build. */
+/* Replaces Engine.__init__ (engine.py:161-179). With tp_size > 1 the context is one rank of a
+ * Megatron tensor-parallel group (the reference models TP only as a duration scale,
+ * cost_model.py:99-100,166, and a lane-equality gate, tp_sync_check, engine.py:50-57): it holds
+ * heads n_heads/tp_size (q) and n_kv_heads/tp_size (k/v), ffn/tp_size, and all-reduces the
+ * o_proj / down_proj partial sums over peer memory. Connect the group with
+ * fp_tp_connect_local (one process) or fp_tp_export + fp_tp_import (one process per GPU)
+ * before creating tasks. nccl_comm must be null (the exchange does not go through NCCL). */
 int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
                   void* nccl_comm, int64_t kv_pages, int32_t page_size, fp_ctx** out);
 int fp_ctx_destroy(fp_ctx* ctx);
@@ -165,6 +171,7 @@ int fp_task_read_kv(fp_ctx* ctx, fp_task* task, int32_t seq, int32_t layer, void
 #define FP_K_DOWN 5
 #define FP_K_LM_HEAD 6
 #define FP_K_RMS_FINAL 7
+#define FP_K_XCHG 8 /* tensor-parallel all-reduce of o_proj / down_proj partials */
 typedef struct fp_prof_rec {
   int32_t kind;  /* FP_K_* */
   int32_t layer;
@@ -179,6 +186,32 @@ int fp_prof_enable(fp_ctx* ctx, int32_t on);
 int fp_prof_collect(fp_ctx* ctx, fp_prof_rec* out, int32_t max, int32_t* n);
 /* Number of kernels this context has launched (guarded no-ops included). */
 int fp_ctx_launch_count(fp_ctx* ctx, int64_t* n);
+
+/* ---- tensor parallelism (config 4: TP = 2/4/8, synchronized operator-boundary preemption) ----
+ * Every rank executes the identical entry list; rank 0 alone evaluates each boundary check and
+ * publishes the decision in a ring the followers read over peer memory, so all ranks stop at the
+ * same entry index (replaces tp_sync_check, engine.py:50-57, used at :254-255).
+ * Only rank 0's fp_signal() is observed by the device. */
+typedef struct fp_tp_handle {
+  char ipc[64];      /* cudaIpcMemHandle_t of the rank's exchange block */
+  int64_t part_rows; /* exchange capacity in token rows (max chunk tokens) */
+  int32_t rank;
+  int32_t device;
+} fp_tp_handle;
+/* One process per GPU: allocate this rank's exchange block (capacity max_tokens rows) and
+ * export it; gather every rank's handle (e.g. torch.distributed.all_gather_object) and pass
+ * them, ordered by rank, to fp_tp_import. */
+int fp_tp_export(fp_ctx* ctx, int64_t max_tokens, fp_tp_handle* out);
+int fp_tp_import(fp_ctx* ctx, const fp_tp_handle* all);
+/* One process: connect ranks 0..n-1. On a single device the ranks share rank 0's stream and
+ * must be driven in lock step through fp_tp_enqueue_lockstep (phase 1 of an entry -- up to the
+ * exchange GEMM -- on every rank before phase 2 on any rank). Destroy followers before rank 0. */
+int fp_tp_connect_local(fp_ctx** ctxs, int32_t n, int64_t max_tokens);
+int fp_tp_enqueue_lockstep(fp_ctx** ctxs, fp_task** tasks, int32_t n, int32_t first,
+                           int32_t last);
+/* Synchronises and reads the rank's device counters: [exchanges, boundaries decided,
+ * gemm ticket, all-reduce ticket] (tickets are 0 between kernels). */
+int fp_ctx_tp_counters(fp_ctx* ctx, int32_t* out4);
 
 /* ---- per-operator entry points (device pointers; unit tests and microbenchmarks) -------- */
 /* C[M,N] = A[M,K] B[N,K]^T; epi: 0 bf16 store, 1 fp32 store, 2 residual add into C (bf16). */

@@ -72,6 +72,9 @@ SHAPES = {
     # small Qwen-style variants for parity tests (vocab not a multiple of 256 on purpose)
     "tiny-qwen3": Shape(2, 512, 4, 2, 128, 1536, 8000, 1e6, 1e-6, qk_norm=True),
     "tiny-qwen2": Shape(2, 512, 4, 2, 128, 1536, 8000, 1e6, 1e-6, qkv_bias=True),
+    # tensor-parallel parity (config 4 family: Qwen2.5 QKV bias, GQA group 5 like Qwen2.5-32B;
+    # TP=4 leaves 5 q heads / 1 kv head per rank and a padded 896-wide qkv shard)
+    "tiny-qwen2-tp": Shape(4, 512, 20, 4, 128, 2048, 8000, 1e6, 1e-6, qkv_bias=True),
 }
 
 

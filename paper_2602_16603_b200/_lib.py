@@ -90,7 +90,18 @@ class ProfRec(C.Structure):
 
 
 KERNEL_KINDS = ("rmsnorm", "qkv_gemm", "attn", "o_gemm", "gate_up_gemm", "down_gemm",
-                "lm_head_gemm", "final_rmsnorm")
+                "lm_head_gemm", "final_rmsnorm", "tp_allreduce")
+
+
+class TpHandle(C.Structure):
+    """fp_tp_handle: one rank's exported exchange block (include/flowprefill.h)."""
+
+    _fields_ = [
+        ("ipc", C.c_char * 64),
+        ("part_rows", C.c_int64),
+        ("rank", C.c_int32),
+        ("device", C.c_int32),
+    ]
 
 # name -> (restype, argtypes)
 _P = C.c_void_p
@@ -123,6 +134,11 @@ _SIGS = {
     "fp_prof_enable": (C.c_int, [_P, _I]),
     "fp_prof_collect": (C.c_int, [_P, C.POINTER(ProfRec), _I, C.POINTER(_I)]),
     "fp_ctx_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "fp_tp_export": (C.c_int, [_P, C.c_int64, C.POINTER(TpHandle)]),
+    "fp_tp_import": (C.c_int, [_P, C.POINTER(TpHandle)]),
+    "fp_tp_connect_local": (C.c_int, [C.POINTER(_P), _I, C.c_int64]),
+    "fp_tp_enqueue_lockstep": (C.c_int, [C.POINTER(_P), C.POINTER(_P), _I, _I, _I]),
+    "fp_ctx_tp_counters": (C.c_int, [_P, C.POINTER(_I)]),
     "fp_op_gemm": (C.c_int, [_P, _I, _P, _P, _P, _I, _I, _I]),
     "fp_op_rmsnorm": (C.c_int, [_P, _P, _P, _P, _I, _I, C.c_float]),
 }

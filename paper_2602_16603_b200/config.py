@@ -57,4 +57,6 @@ SHAPES = {
                              qk_norm=True),
     "tiny-qwen2": ModelShape("tiny-qwen2", 2, 512, 4, 2, 128, 1536, 8000, 1e6, 1e-6,
                              qkv_bias=True),
+    "tiny-qwen2-tp": ModelShape("tiny-qwen2-tp", 4, 512, 20, 4, 128, 2048, 8000, 1e6, 1e-6,
+                                qkv_bias=True),
 }

@@ -277,6 +277,22 @@ DEVI int ld_volatile_sys(const volatile int* p) {
   asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+DEVI unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+DEVI void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// 16-byte load cached in L2 only (peer memory written by another GPU between kernels)
+DEVI uint4 ld_cg_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 // Programmatic dependent launch: wait until the preceding kernel in the stream has completed
 // and its memory is visible (no-op when the launch was not programmatic).
 DEVI void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -30,6 +30,40 @@ struct TaskCtl {
   int dec[1];       // [n_entries]: 0 undecided, 1 go, 2 stop
 };
 
+// ---- tensor parallelism: cross-rank state -------------------------------------------------
+// The reference keeps TP as one logical lane whose boundary is "synchronised" by a lane-counter
+// equality check (tp_sync_check, prefillsim/engine.py:50-57, used at :254-255; the paper's
+// synchronized iteration counter). Here every rank runs the identical entry list
+// and rank 0 alone decides each boundary; followers adopt rank 0's decision from its ring, so
+// all ranks stop at the same entry by construction.
+constexpr int kTpMax = 8;
+constexpr int kTpRing = 64;
+
+// Per-rank block in peer-visible (IPC-shareable) device memory.
+struct TpShared {
+  unsigned long long ready;             // exchange GEMMs whose partial sum is complete
+  unsigned long long pad0[15];
+  unsigned long long ring[kTpRing];     // rank 0 only: ((boundary + 1) << 2) | decision
+};
+
+// Per-rank device-local counters (identical sequences on every rank: only entries that
+// actually execute advance them, and all ranks execute the same entries).
+struct TpLocal {
+  int xcount;    // exchanges (o_proj / down_proj all-reduces) completed
+  int gemm_ctr;  // CTA completion ticket of the current exchange GEMM
+  int ar_ctr;    // CTA completion ticket of the current all-reduce
+  int bcount;    // boundaries decided
+  int pad[28];
+};
+
+struct TpDev {
+  int rank, size;
+  long long part_rows;                  // capacity (token rows) of each partial buffer
+  TpLocal* local;
+  TpShared* peer[kTpMax];               // every rank's shared block (peer[rank] = own)
+  __nv_bfloat16* part[kTpMax][2];       // every rank's double-buffered partial [rows, hidden]
+};
+
 struct Guard {
   HostCtl* host;  // device alias of the mapped control block (may be null: unguarded)
   TaskCtl* task;  // null: unguarded launch (per-op unit entry points)
@@ -39,6 +73,7 @@ struct Guard {
   int first;     // 1 for the first kernel of the entry: evaluates the check
   int eligible;  // the boundary in front of this entry is preemption-eligible
   int pad;
+  const TpDev* tp;  // null unless tensor parallel
 };
 
 constexpr int kDecGo = 1;
@@ -67,9 +102,30 @@ DEVI bool guard_pass(const Guard& g) {
     decider = true;
   }
   int want = kDecGo;
-  if (g.eligible && g.host != nullptr && ld_volatile_sys(&g.host->signal)) want = kDecStop;
+  const TpDev* tp = g.tp;
+  const int b = tp ? *(volatile int*)&tp->local->bcount : 0;
+  if (tp && tp->rank != 0) {
+    // follower: adopt rank 0's decision for this boundary (same boundary count on every rank)
+    const unsigned long long* ring = &tp->peer[0]->ring[b % kTpRing];
+    for (;;) {
+      if ((d = *slot)) return d == kDecGo;  // another CTA of this kernel already decided
+      const unsigned long long v = ld_acquire_sys_u64(ring);
+      if ((long long)(v >> 2) == b + 1) {  // tags are boundary + 1 (0 = never written)
+        want = (int)(v & 3);
+        break;
+      }
+      __nanosleep(64);
+    }
+  } else if (g.eligible && g.host != nullptr && ld_volatile_sys(&g.host->signal)) {
+    want = kDecStop;
+  }
   const int old = atomicCAS(&g.task->dec[g.entry], 0, want);
   d = old ? old : want;
+  if (old == 0 && tp) {
+    if (tp->rank == 0)
+      st_release_sys_u64(&tp->peer[0]->ring[b % kTpRing], ((unsigned long long)(b + 1) << 2) | d);
+    tp->local->bcount = b + 1;
+  }
   if (old == 0 && d == kDecStop) {  // later launches of this generation become no-ops
     *sg = g.gen;                    // (they start only after this kernel has exited)
     __threadfence();
@@ -90,6 +146,19 @@ DEVI bool guard_pass(const Guard& g) {
     }
   }
   return d == kDecGo;
+}
+
+// Thread 0 of every CTA of an exchange GEMM, after the CTA's partial-sum stores: the last CTA
+// to finish publishes "partial of exchange xcount complete" to the peers.
+DEVI void tp_publish_partial(const TpDev* tp) {
+  __threadfence_system();
+  const int xc = *(volatile int*)&tp->local->xcount;
+  const int old = atomicAdd(&tp->local->gemm_ctr, 1);
+  if (old == (int)(gridDim.x * gridDim.y * gridDim.z) - 1) {
+    tp->local->gemm_ctr = 0;
+    __threadfence_system();
+    st_release_sys_u64(&tp->peer[tp->rank]->ready, (unsigned long long)xc + 1);
+  }
 }
 
 // Block-wide wrapper; every thread calls it.

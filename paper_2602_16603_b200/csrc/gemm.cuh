@@ -55,6 +55,8 @@ struct GemmParams {
   int full_tiles;
   float* ws;
   int* tickets;
+  int xchg;  // tensor parallel o_proj/down_proj: store the partial sum into this rank's exchange
+  int pad3;  // buffer (EPI_STORE_BF16) and publish it to the peers (tp_publish_partial)
   Guard guard;
 };
 
@@ -375,6 +377,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       } else if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32) {
+        void* out = p.out;
+        if (EPI == EPI_STORE_BF16 && p.xchg) {
+          const TpDev* tp = p.guard.tp;
+          out = tp->part[tp->rank][tp->local->xcount & 1];
+        }
         if (splits == 1) {
           mbar_wait(&tfull[acc], acc_ph);
           tc_fence_after();
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           load32(c * 32, v);
           if (live) {
             if constexpr (EPI == EPI_STORE_F32) {
-              float* dst = reinterpret_cast<float*>(p.out) + (long long)m * p.ldo + n0 + c * 32;
+              float* dst = reinterpret_cast<float*>(out) + (long long)m * p.ldo + n0 + c * 32;
 #pragma unroll
               for (int i = 0; i < 8; ++i)
                 st_global_v4(dst + 4 * i,
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                         __float_as_uint(v[4 * i + 3])));
             } else {
               __nv_bfloat16* dst =
-                  reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)m * p.ldo + n0 + c * 32;
+                  reinterpret_cast<__nv_bfloat16*>(out) + (long long)m * p.ldo + n0 + c * 32;
               store_row32_bf16(dst, v);
             }
           }
@@ -437,6 +444,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int hh = 0; hh < BN / 128; ++hh) {
           const int col0 = n0 + hh * 128;
+          if (col0 >= p.q_cols + 2 * p.kv_cols) continue;  // zero padding of the qkv width
           const bool is_q = col0 < p.q_cols;
           const bool is_v = col0 >= p.q_cols + p.kv_cols;
           __nv_bfloat16* dst;
@@ -508,11 +516,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if (splits == 1) release_acc(acc);
     }
+    if (EPI == EPI_STORE_BF16 && p.xchg) __threadfence_system();  // partials visible to peers
   }
 
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/arrivals are all done
   else __syncthreads();
+  if (EPI == EPI_STORE_BF16 && p.xchg && run && threadIdx.x == 0) tp_publish_partial(p.guard.tp);
   if (warp == 2) {
     tc_fence_after();
     if constexpr (CG == 2) tmem_dealloc_2sm<Cfg::TMEM_COLS>(tbase);

@@ -19,6 +19,7 @@
 #include "control.cuh"
 #include "gemm.cuh"
 #include "norm.cuh"
+#include "xchg.cuh"
 
 using namespace fp;
 
@@ -134,8 +135,21 @@ struct Task {
 struct fp_ctx {
   int device = 0, num_sms = 148;
   fp_model_cfg cfg{};
+  // this rank's shard (tp_size == 1: the whole model). qkv_n is padded to the 256-wide GEMM
+  // tile; the padding rows of Wqkv are zero and the QKV epilogue skips them.
+  int hq = 0, hkv = 0, ffn = 0;
   int qdim = 0, kvdim = 0, qkv_n = 0, vocab_pad = 0;
+  int tp_rank = 0, tp_size = 1;
   cudaStream_t stream = nullptr, upload = nullptr;
+  cudaStream_t own_stream = nullptr;  // lock-step TP groups share rank 0's stream
+  // tensor parallel exchange (null when tp_size == 1)
+  TpDev tp_host{};
+  TpDev* d_tp = nullptr;      // device copy of tp_host
+  TpLocal* tp_local = nullptr;
+  char* tp_block = nullptr;   // own IPC-shareable block: TpShared | part[0] | part[1]
+  std::vector<void*> tp_opened;  // peer blocks opened through IPC
+  bool tp_connected = false;
+  bool tp_lockstep = false;
   std::vector<Layer> layers;
   __nv_bfloat16 *embed = nullptr, *final_g = nullptr, *lm_head = nullptr;
   CUtensorMap tm_lm;
@@ -362,8 +376,12 @@ static bool boundary_eligible(const fp_ctx* c, int gran, int i, int n_entries) {
   return false;
 }
 
-// Enqueue the kernels of one timeline entry. Caller holds launch_mu.
-static int launch_entry(fp_ctx* c, Task* t, int e) {
+// Enqueue the kernels of one timeline entry. Caller holds launch_mu. Tensor parallel
+// o_proj/down_proj entries have two phases: the exchange GEMM (phase 1) and the all-reduce plus
+// anything after it (phase 2); a lock-step group on one device launches phase 1 of every rank
+// before phase 2 of any rank so no all-reduce waits on a kernel queued behind it.
+constexpr int kPhasePre = 1, kPhasePost = 2, kPhaseAll = 3;
+static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
   const fp_model_cfg& m = c->cfg;
   const int L = m.num_layers;
   const int ci = e / (5 * L);
@@ -382,6 +400,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
   g.task_id = t->id;
   g.first = 1;
   g.eligible = (e != t->seg_first) && boundary_eligible(c, t->granularity, e - 1, t->n_entries);
+  g.tp = c->d_tp;
   Guard g2 = g;
   g2.first = 0;
 
@@ -390,6 +409,8 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
   const int* tpage = t->d_tpage + ch.tok0;
   __nv_bfloat16* kv_layer = c->kv + (long long)layer * c->kv_pages * c->page_elems;
 
+  const bool xchg_op = c->tp_size > 1 && (op == FP_OP_O_PROJ || op == FP_OP_DOWN_PROJ);
+  if (!xchg_op && !(phase & kPhasePre)) return FP_OK;  // single-phase entries run in phase 1
   if (op == FP_OP_QKV_PROJ || op == FP_OP_GATE_UP_PROJ) {
     RmsParams r{};
     r.M = M;
@@ -427,7 +448,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
       p.q_cols = c->qdim;
       p.kv_cols = c->kvdim;
       p.page_size = c->page_size;
-      p.n_kv_heads = m.n_kv_heads;
+      p.n_kv_heads = c->hkv;
       p.bias = ly.bqkv;
       p.q_norm = ly.q_norm;
       p.k_norm = ly.k_norm;
@@ -435,9 +456,9 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
       ProfScope ps(c, st, FP_K_QKV, layer, M, 2.0 * M * p.N * p.K, 0.0);
       launch_gemm<EPI_QKV>(c, t->tm_xn, ly.tm_qkv, p, st);
     } else {
-      p.N = 2 * m.ffn;
+      p.N = 2 * c->ffn;
       p.out = t->act;
-      p.ldo = m.ffn;
+      p.ldo = c->ffn;
       ProfScope ps(c, st, FP_K_GATE_UP, layer, M, 2.0 * M * p.N * p.K, 0.0);
       launch_gemm<EPI_SWIGLU>(c, t->tm_xn, ly.tm_gu, p, st);
     }
@@ -445,38 +466,55 @@ static int launch_entry(fp_ctx* c, Task* t, int e) {
     AttnTcParams a{};
     a.items = t->d_items + ch.item0;
     a.n_items = ch.n_items;
-    a.n_heads = m.n_heads;
-    a.n_kv_heads = m.n_kv_heads;
-    a.pairs_per_kv = (m.n_heads / m.n_kv_heads + 1) / 2;
+    a.n_heads = c->hq;
+    a.n_kv_heads = c->hkv;
+    a.pairs_per_kv = (c->hq / c->hkv + 1) / 2;
     a.out = t->ao;
     a.ldo = c->qdim;
     a.block_table = t->d_bt;
     a.bt_stride = t->bt_stride;
-    a.kv_row_layer = (long long)layer * c->kv_pages * 2 * m.n_kv_heads * c->page_size;
-    a.kv_rows_per_page = 2 * m.n_kv_heads * c->page_size;
+    a.kv_row_layer = (long long)layer * c->kv_pages * 2 * c->hkv * c->page_size;
+    a.kv_rows_per_page = 2 * c->hkv * c->page_size;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)m.head_dim);
     a.guard = g;
     if (a.n_items > 0) {
       ProfScope ps(c, st, FP_K_ATTN, layer, M, ch.attn_flops, 0.0);
       launch_attn(t->tm_q, c->tm_kv, a, st);
     }
-  } else {  // O_PROJ / DOWN_PROJ: residual add
+  } else {  // O_PROJ / DOWN_PROJ: residual add (tensor parallel: partial sum + all-reduce)
     GemmParams p{};
     p.M = M;
     p.N = m.hidden;
     p.resid = t->h;
     p.ldr = m.hidden;
     p.guard = g;
-    if (op == FP_OP_O_PROJ) {
-      p.K = c->qdim;
-      ProfScope ps(c, st, FP_K_O, layer, M, 2.0 * M * p.N * p.K, 0.0);
-      launch_gemm<EPI_RESID>(c, t->tm_ao, ly.tm_o, p, st);
+    p.K = op == FP_OP_O_PROJ ? c->qdim : c->ffn;
+    const CUtensorMap& ta = op == FP_OP_O_PROJ ? t->tm_ao : t->tm_act;
+    const CUtensorMap& tb = op == FP_OP_O_PROJ ? ly.tm_o : ly.tm_d;
+    const int kind = op == FP_OP_O_PROJ ? FP_K_O : FP_K_DOWN;
+    if (!xchg_op) {
+      ProfScope ps(c, st, kind, layer, M, 2.0 * M * p.N * p.K, 0.0);
+      launch_gemm<EPI_RESID>(c, ta, tb, p, st);
     } else {
-      p.K = m.ffn;
-      {
-        ProfScope ps(c, st, FP_K_DOWN, layer, M, 2.0 * M * p.N * p.K, 0.0);
-        launch_gemm<EPI_RESID>(c, t->tm_act, ly.tm_d, p, st);
+      if (phase & kPhasePre) {
+        p.xchg = 1;
+        p.ldo = m.hidden;
+        ProfScope ps(c, st, kind, layer, M, 2.0 * M * p.N * p.K, 0.0);
+        launch_gemm<EPI_STORE_BF16>(c, ta, tb, p, st);
       }
+      if (!(phase & kPhasePost)) return FP_OK;
+      XchgParams x{};
+      x.M = M;
+      x.d = m.hidden;
+      x.h = t->h;
+      x.ldh = m.hidden;
+      x.guard = g2;
+      const long long vecs = (long long)M * m.hidden / 8;
+      const int grid = (int)std::max(1LL, std::min<long long>((vecs + 255) / 256, 8LL * c->num_sms));
+      ProfScope ps(c, st, FP_K_XCHG, layer, M, 0.0, (double)(c->tp_size + 2) * M * m.hidden * 2);
+      launch_pdl(tp_allreduce_kernel, dim3(grid), dim3(256), 0, st, x);
+    }
+    if (op == FP_OP_DOWN_PROJ) {
       if (layer == L - 1 && ch.n_last > 0) {  // completion: final norm + lm_head of last tokens
         RmsParams r{};
         r.M = ch.n_last;
@@ -553,14 +591,16 @@ int fp_version(void) { return 1; }
 
 int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
                   void* nccl_comm, int64_t kv_pages, int32_t page_size, fp_ctx** out) {
-  (void)tp_rank;
-  (void)nccl_comm;
   REQ(cfg && out, "null argument");
-  REQ(tp_size == 1, "tensor parallelism is not built into this library version");
+  REQ(nccl_comm == nullptr,
+      "nccl_comm must be null: the tensor-parallel exchange runs over peer memory "
+      "(fp_tp_connect_local / fp_tp_export + fp_tp_import)");
+  REQ(tp_size >= 1 && tp_size <= kTpMax && tp_rank >= 0 && tp_rank < tp_size, "bad tp_rank/tp_size");
   REQ(cfg->head_dim == 128, "head_dim must be 128");
-  REQ(cfg->hidden % 256 == 0 && cfg->ffn % 128 == 0, "hidden%256 and ffn%128 required");
   REQ(cfg->n_heads % cfg->n_kv_heads == 0, "n_heads must be a multiple of n_kv_heads");
-  REQ(((cfg->n_heads + 2 * cfg->n_kv_heads) * 128) % 256 == 0, "qkv width must be %256");
+  REQ(cfg->n_kv_heads % tp_size == 0, "n_kv_heads must be divisible by tp_size");
+  REQ(cfg->hidden % 256 == 0 && cfg->ffn % (128 * tp_size) == 0,
+      "hidden%256 and ffn%(128*tp_size) required");
   REQ(page_size == 128, "page_size must be 128 (one attention KV tile per page)");
   REQ(kv_pages > 0, "kv_pages must be > 0");
   CK(cudaSetDevice(device));
@@ -570,14 +610,20 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   fp_ctx* c = new fp_ctx();
   c->device = device;
   c->cfg = *cfg;
-  c->qdim = cfg->n_heads * 128;
-  c->kvdim = cfg->n_kv_heads * 128;
-  c->qkv_n = c->qdim + 2 * c->kvdim;
+  c->tp_rank = tp_rank;
+  c->tp_size = tp_size;
+  c->hq = cfg->n_heads / tp_size;
+  c->hkv = cfg->n_kv_heads / tp_size;
+  c->ffn = cfg->ffn / tp_size;
+  c->qdim = c->hq * 128;
+  c->kvdim = c->hkv * 128;
+  c->qkv_n = (c->qdim + 2 * c->kvdim + 255) / 256 * 256;
   c->page_size = page_size;
   c->kv_pages = kv_pages;
-  c->page_elems = 2LL * cfg->n_kv_heads * page_size * 128;
+  c->page_elems = 2LL * c->hkv * page_size * 128;
   CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = c->stream;
   CK(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
   // let the async mempool keep freed task workspaces
   cudaMemPool_t pool;
@@ -590,9 +636,10 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   for (int l = 0; l < L; ++l) {
     Layer& ly = c->layers[l];
     CK(cudaMalloc(&ly.wqkv, (size_t)c->qkv_n * d * 2));
+    CK(cudaMemset(ly.wqkv, 0, (size_t)c->qkv_n * d * 2));  // padding rows stay zero
     CK(cudaMalloc(&ly.wo, (size_t)d * c->qdim * 2));
-    CK(cudaMalloc(&ly.wgu, (size_t)2 * cfg->ffn * d * 2));
-    CK(cudaMalloc(&ly.wd, (size_t)d * cfg->ffn * 2));
+    CK(cudaMalloc(&ly.wgu, (size_t)2 * c->ffn * d * 2));
+    CK(cudaMalloc(&ly.wd, (size_t)d * c->ffn * 2));
     CK(cudaMalloc(&ly.attn_g, (size_t)d * 2));
     CK(cudaMalloc(&ly.ffn_g, (size_t)d * 2));
     if (cfg->qkv_bias) {
@@ -606,8 +653,8 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     int rc;
     if ((rc = make_map(&ly.tm_qkv, ly.wqkv, c->qkv_n, d, 128))) return rc;
     if ((rc = make_map(&ly.tm_o, ly.wo, d, c->qdim, 128))) return rc;
-    if ((rc = make_map(&ly.tm_gu, ly.wgu, 2 * cfg->ffn, d, 128))) return rc;
-    if ((rc = make_map(&ly.tm_d, ly.wd, d, cfg->ffn, 128))) return rc;
+    if ((rc = make_map(&ly.tm_gu, ly.wgu, 2 * c->ffn, d, 128))) return rc;
+    if ((rc = make_map(&ly.tm_d, ly.wd, d, c->ffn, 128))) return rc;
   }
   CK(cudaMalloc(&c->embed, (size_t)cfg->vocab * d * 2));
   c->vocab_pad = (cfg->vocab + 255) / 256 * 256;  // lm_head GEMM tiles are 256 wide
@@ -638,7 +685,7 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     if (const char* e = getenv("FP_PAIR_GEMM")) c->use_pair_gemm = atoi(e) != 0;
     if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
-    const uint64_t rows = (uint64_t)L * kv_pages * 2 * cfg->n_kv_heads * page_size;
+    const uint64_t rows = (uint64_t)L * kv_pages * 2 * c->hkv * page_size;
     REQ(rows < (1ull << 31), "KV pool too large for 32-bit TMA row coordinates");
     int rc = make_map(&c->tm_kv, c->kv, rows, 128, 128);
     if (rc) return rc;
@@ -666,7 +713,8 @@ int fp_ctx_destroy(fp_ctx* c) {
   c->wcv.notify_all();
   if (c->worker.joinable()) c->worker.join();
   cudaSetDevice(c->device);
-  cudaStreamSynchronize(c->stream);
+  if (c->tp_lockstep) cudaDeviceSynchronize();  // the shared stream may belong to rank 0
+  else cudaStreamSynchronize(c->stream);
   for (auto& ly : c->layers) {
     cudaFree(ly.wqkv);
     cudaFree(ly.wo);
@@ -686,9 +734,13 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaFree(c->ws);
   cudaFree(c->tickets);
   cudaFreeHost((void*)c->hctl);
+  for (void* ptr : c->tp_opened) cudaIpcCloseMemHandle(ptr);
+  cudaFree(c->tp_block);
+  cudaFree(c->tp_local);
+  cudaFree(c->d_tp);
   if (c->stage) cudaFreeHost(c->stage);
   if (c->stage_ev) cudaEventDestroy(c->stage_ev);
-  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->own_stream);
   cudaStreamDestroy(c->upload);
   delete c;
   return FP_OK;
@@ -717,33 +769,9 @@ int fp_sync(fp_ctx* c) {
   return FP_OK;
 }
 
-static __nv_bfloat16* weight_ptr(fp_ctx* c, int tensor, int layer, long long* n_out,
-                                 long long* off) {
-  const fp_model_cfg& m = c->cfg;
-  const long long d = m.hidden;
-  *off = 0;
-  Layer* ly = (layer >= 0 && layer < m.num_layers) ? &c->layers[layer] : nullptr;
-  switch (tensor) {
-    case FP_W_EMBED: *n_out = (long long)m.vocab * d; return c->embed;
-    case FP_W_LM_HEAD: *n_out = (long long)m.vocab * d; return c->lm_head;
-    case FP_W_FINAL_NORM: *n_out = d; return c->final_g;
-    default: break;
-  }
-  if (!ly) return nullptr;
-  switch (tensor) {
-    case FP_W_Q: *n_out = c->qdim * d; return ly->wqkv;
-    case FP_W_K: *n_out = c->kvdim * d; *off = c->qdim * d; return ly->wqkv;
-    case FP_W_V: *n_out = c->kvdim * d; *off = (c->qdim + c->kvdim) * d; return ly->wqkv;
-    case FP_W_O: *n_out = d * c->qdim; return ly->wo;
-    case FP_W_GATE: *n_out = (long long)m.ffn * d; return ly->wgu;
-    case FP_W_UP: *n_out = (long long)m.ffn * d; return ly->wgu;
-    case FP_W_DOWN: *n_out = d * m.ffn; return ly->wd;
-    case FP_W_ATTN_NORM: *n_out = d; return ly->attn_g;
-    case FP_W_FFN_NORM: *n_out = d; return ly->ffn_g;
-  }
-  return nullptr;
-}
-
+// Weights arrive as the full (unsharded) canonical tensors; a tensor-parallel rank keeps its
+// Megatron shard: q/k/v/gate/up rows (column-parallel), o/down columns (row-parallel), biases
+// with their rows, everything else replicated.
 // bf16 host vector -> fp32 device vector (biases, q/k norm weights live in fp32)
 static int load_f32_vec(float* dst, const void* host, int64_t n) {
   std::vector<float> f(n);
@@ -759,37 +787,84 @@ static int load_f32_vec(float* dst, const void* host, int64_t n) {
 int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, int64_t n) {
   REQ(c && host, "null argument");
   CK(cudaSetDevice(c->device));
-  if (tensor >= FP_W_Q_BIAS && tensor <= FP_W_K_NORM) {
-    REQ(layer >= 0 && layer < c->cfg.num_layers, "bad layer");
-    Layer& ly = c->layers[layer];
-    if (tensor <= FP_W_V_BIAS) {
-      REQ(ly.bqkv != nullptr, "model has no qkv bias");
-      const long long off = tensor == FP_W_Q_BIAS ? 0 : (tensor == FP_W_K_BIAS ? c->qdim : c->qdim + c->kvdim);
-      REQ(n == (tensor == FP_W_Q_BIAS ? c->qdim : c->kvdim), "bias size mismatch");
-      return load_f32_vec(ly.bqkv + off, host, n);
+  const fp_model_cfg& m = c->cfg;
+  const long long d = m.hidden, r = c->tp_rank;
+  const long long Qd = (long long)m.n_heads * 128, KVd = (long long)m.n_kv_heads * 128;
+  const long long F = m.ffn;
+  const char* src = static_cast<const char*>(host);
+  switch (tensor) {  // replicated, model-level
+    case FP_W_EMBED:
+    case FP_W_LM_HEAD:
+      REQ(n == (long long)m.vocab * d, "weight size mismatch");
+      CK(cudaMemcpy(tensor == FP_W_EMBED ? c->embed : c->lm_head, host, (size_t)n * 2,
+                    cudaMemcpyHostToDevice));
+      return FP_OK;
+    case FP_W_FINAL_NORM:
+      REQ(n == d, "weight size mismatch");
+      CK(cudaMemcpy(c->final_g, host, (size_t)n * 2, cudaMemcpyHostToDevice));
+      return FP_OK;
+    default:
+      break;
+  }
+  REQ(layer >= 0 && layer < m.num_layers, "bad layer");
+  Layer& ly = c->layers[layer];
+  switch (tensor) {
+    case FP_W_Q:
+    case FP_W_K:
+    case FP_W_V: {  // column-parallel: this rank's head rows
+      const bool q = tensor == FP_W_Q;
+      REQ(n == (q ? Qd : KVd) * d, "weight size mismatch");
+      const long long rows = q ? c->qdim : c->kvdim;
+      const long long off = q ? 0 : (tensor == FP_W_K ? c->qdim : c->qdim + c->kvdim);
+      CK(cudaMemcpy(ly.wqkv + off * d, src + r * rows * d * 2, (size_t)rows * d * 2,
+                    cudaMemcpyHostToDevice));
+      return FP_OK;
     }
-    REQ(ly.q_norm != nullptr, "model has no q/k norm");
-    REQ(n == 128, "q/k norm size must be head_dim");
-    return load_f32_vec(tensor == FP_W_Q_NORM ? ly.q_norm : ly.k_norm, host, n);
+    case FP_W_O:
+    case FP_W_DOWN: {  // row-parallel: this rank's input columns
+      const bool o = tensor == FP_W_O;
+      const long long full = o ? Qd : F, cols = o ? c->qdim : c->ffn;
+      REQ(n == d * full, "weight size mismatch");
+      CK(cudaMemcpy2D(o ? ly.wo : ly.wd, (size_t)cols * 2, src + r * cols * 2, (size_t)full * 2,
+                      (size_t)cols * 2, (size_t)d, cudaMemcpyHostToDevice));
+      return FP_OK;
+    }
+    case FP_W_GATE:
+    case FP_W_UP: {
+      // this rank's ffn rows, packed gate/up interleaved in blocks of 128 rows:
+      // [g(128) | u(128)] per 256-row block, so one 256-wide GEMM tile holds matching gate and
+      // up columns (SwiGLU epilogue).
+      REQ(n == F * d, "weight size mismatch");
+      const int half = tensor == FP_W_UP ? 1 : 0;
+      const char* base = src + r * c->ffn * d * 2;
+      for (int b = 0; b < c->ffn / 128; ++b)
+        CK(cudaMemcpy(ly.wgu + ((size_t)b * 256 + half * 128) * d, base + (size_t)b * 128 * d * 2,
+                      (size_t)128 * d * 2, cudaMemcpyHostToDevice));
+      return FP_OK;
+    }
+    case FP_W_ATTN_NORM:
+    case FP_W_FFN_NORM:
+      REQ(n == d, "weight size mismatch");
+      CK(cudaMemcpy(tensor == FP_W_ATTN_NORM ? ly.attn_g : ly.ffn_g, host, (size_t)n * 2,
+                    cudaMemcpyHostToDevice));
+      return FP_OK;
+    case FP_W_Q_BIAS:
+    case FP_W_K_BIAS:
+    case FP_W_V_BIAS: {
+      REQ(ly.bqkv != nullptr, "model has no qkv bias");
+      const bool q = tensor == FP_W_Q_BIAS;
+      REQ(n == (q ? Qd : KVd), "bias size mismatch");
+      const long long rows = q ? c->qdim : c->kvdim;
+      const long long off = q ? 0 : (tensor == FP_W_K_BIAS ? c->qdim : c->qdim + c->kvdim);
+      return load_f32_vec(ly.bqkv + off, src + r * rows * 2, rows);
+    }
+    case FP_W_Q_NORM:
+    case FP_W_K_NORM:
+      REQ(ly.q_norm != nullptr, "model has no q/k norm");
+      REQ(n == 128, "q/k norm size must be head_dim");
+      return load_f32_vec(tensor == FP_W_Q_NORM ? ly.q_norm : ly.k_norm, host, n);
   }
-  long long need = 0, off = 0;
-  __nv_bfloat16* dst = weight_ptr(c, tensor, layer, &need, &off);
-  REQ(dst != nullptr, "unknown tensor/layer");
-  REQ(n == need, "weight size mismatch");
-  if (tensor == FP_W_GATE || tensor == FP_W_UP) {
-    // pack gate/up interleaved in blocks of 128 rows: [g(128) | u(128)] per 256-row block,
-    // so one 256-wide GEMM tile holds matching gate and up columns (SwiGLU epilogue).
-    const int d = c->cfg.hidden;
-    const int blocks = c->cfg.ffn / 128;
-    const char* src = static_cast<const char*>(host);
-    const int half = tensor == FP_W_UP ? 1 : 0;
-    for (int b = 0; b < blocks; ++b)
-      CK(cudaMemcpy(dst + ((size_t)b * 256 + half * 128) * d, src + (size_t)b * 128 * d * 2,
-                    (size_t)128 * d * 2, cudaMemcpyHostToDevice));
-  } else {
-    CK(cudaMemcpy(dst + off, host, (size_t)n * 2, cudaMemcpyHostToDevice));
-  }
-  return FP_OK;
+  return set_err(FP_ERR_ARG, "unknown tensor");
 }
 
 int fp_weights_init_random(fp_ctx* c, uint64_t seed, float stdv) {
@@ -798,22 +873,24 @@ int fp_weights_init_random(fp_ctx* c, uint64_t seed, float stdv) {
   const fp_model_cfg& m = c->cfg;
   const long long d = m.hidden;
   uint64_t s = seed * 1000003ull;
-  auto fill = [&](__nv_bfloat16* p, long long n, float mean, float sd) {
-    init_normal_kernel<<<1184, 256, 0, c->stream>>>(p, n, s++, mean, sd);
+  // replicated tensors draw the same stream on every rank; shards mix in the rank
+  const uint64_t shard = (uint64_t)c->tp_rank * 0x9E3779B97F4A7C15ull;
+  auto fill = [&](__nv_bfloat16* p, long long n, float mean, float sd, bool sharded = false) {
+    init_normal_kernel<<<1184, 256, 0, c->stream>>>(p, n, (s++) ^ (sharded ? shard : 0), mean, sd);
   };
   fill(c->embed, (long long)m.vocab * d, 0.f, stdv);
   fill(c->lm_head, (long long)m.vocab * d, 0.f, stdv);
   fill(c->final_g, d, 1.f, 0.1f);
   for (auto& ly : c->layers) {
-    fill(ly.wqkv, (long long)c->qkv_n * d, 0.f, stdv);
-    fill(ly.wo, d * c->qdim, 0.f, stdv);
-    fill(ly.wgu, 2LL * m.ffn * d, 0.f, stdv);
-    fill(ly.wd, d * m.ffn, 0.f, stdv);
+    fill(ly.wqkv, (long long)(c->qdim + 2 * c->kvdim) * d, 0.f, stdv, true);
+    fill(ly.wo, d * c->qdim, 0.f, stdv, true);
+    fill(ly.wgu, 2LL * c->ffn * d, 0.f, stdv, true);
+    fill(ly.wd, d * c->ffn, 0.f, stdv, true);
     fill(ly.attn_g, d, 1.f, 0.1f);
     fill(ly.ffn_g, d, 1.f, 0.1f);
     if (ly.bqkv || ly.q_norm) {
-      std::vector<float> v(c->qkv_n);
-      for (int i = 0; i < c->qkv_n; ++i) v[i] = 0.02f * (float)((int)((s * 2654435761ull + i * 40503ull) % 2001) - 1000) / 1000.f;
+      std::vector<float> v(c->qkv_n, 0.f);
+      for (int i = 0; i < c->qdim + 2 * c->kvdim; ++i) v[i] = 0.02f * (float)((int)((s * 2654435761ull + i * 40503ull) % 2001) - 1000) / 1000.f;
       if (ly.bqkv) CK(cudaMemcpy(ly.bqkv, v.data(), c->qkv_n * 4, cudaMemcpyHostToDevice));
       for (int i = 0; i < 128; ++i) v[i] = 1.f + 5.f * v[i];
       if (ly.q_norm) CK(cudaMemcpy(ly.q_norm, v.data(), 512, cudaMemcpyHostToDevice));
@@ -853,6 +930,17 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
     total += lens[i];
   }
   t->total = (int)total;
+  if (c->tp_size > 1) {
+    const long long max_chunk = (chunk_tokens == 0 || chunk_tokens >= total) ? total : chunk_tokens;
+    const char* why = !c->tp_connected ? "tensor-parallel context is not connected to its peers"
+                      : max_chunk > c->tp_host.part_rows
+                          ? "chunk exceeds the tensor-parallel exchange capacity (use chunk_tokens)"
+                          : nullptr;
+    if (why) {
+      delete t;
+      return set_err(FP_ERR_STATE, why);
+    }
+  }
   for (long long i = 0; i < total; ++i)
     if (ids[i] < 0 || ids[i] >= m.vocab) {
       delete t;
@@ -985,7 +1073,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   CK(cudaMallocAsync((void**)&t->xn, M * d * 2, up));
   CK(cudaMallocAsync((void**)&t->q, M * c->qdim * 2, up));
   CK(cudaMallocAsync((void**)&t->ao, M * c->qdim * 2, up));
-  CK(cudaMallocAsync((void**)&t->act, M * (long long)m.ffn * 2, up));
+  CK(cudaMallocAsync((void**)&t->act, M * (long long)c->ffn * 2, up));
   CK(cudaMallocAsync((void**)&t->xf, (long long)n_seqs * d * 2, up));
   CK(cudaMallocAsync((void**)&t->logits, (long long)n_seqs * c->vocab_pad * 4, up));
   CK(cudaMemsetAsync(t->logits, 0, (long long)n_seqs * c->vocab_pad * 4, up));
@@ -996,7 +1084,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   int rc;
   if ((rc = make_map(&t->tm_xn, t->xn, M, d, 128))) return rc;
   if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
-  if ((rc = make_map(&t->tm_act, t->act, M, m.ffn, 128))) return rc;
+  if ((rc = make_map(&t->tm_act, t->act, M, c->ffn, 128))) return rc;
   if ((rc = make_map(&t->tm_xf, t->xf, n_seqs, d, 128))) return rc;
   if ((rc = make_map(&t->tm_q, t->q, M, c->qdim, 128))) return rc;
   CK(cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming));
@@ -1107,6 +1195,7 @@ int fp_task_enqueue(fp_ctx* c, fp_task* task, int32_t first, int32_t last) {
 
 int fp_task_start(fp_ctx* c, fp_task* task, int32_t first) {
   Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && !c->tp_lockstep, "lock-step tensor-parallel groups launch through fp_tp_enqueue_lockstep");
   int rc = fp_task_begin_segment(c, task, first);
   if (rc) return rc;
   for (int spin = 0;; ++spin) {  // a stopped segment's worker is still winding down
@@ -1192,7 +1281,7 @@ int fp_task_read_kv(fp_ctx* c, fp_task* task, int32_t seq, int32_t layer, void* 
   REQ(seq >= 0 && seq < t->n_seqs && layer >= 0 && layer < c->cfg.num_layers, "bad seq/layer");
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
-  const int PS = c->page_size, H = c->cfg.n_kv_heads, n = t->lens[seq];
+  const int PS = c->page_size, H = c->hkv, n = t->lens[seq];
   int page_base = 0;
   for (int i = 0; i < seq; ++i) page_base += (t->lens[i] + PS - 1) / PS;
   std::vector<__nv_bfloat16> page((size_t)c->page_elems);
@@ -1292,6 +1381,172 @@ int fp_op_rmsnorm(fp_ctx* c, const void* x, const void* gamma, void* out, int32_
   int rc = launch_rms(r, c->stream);
   if (rc) return rc;
   CK(cudaGetLastError());
+  return FP_OK;
+}
+
+// ---- tensor parallelism -----------------------------------------------------------------
+static size_t tp_header_bytes() { return (sizeof(TpShared) + 4095) / 4096 * 4096; }
+
+static int tp_alloc_block(fp_ctx* c, int64_t max_tokens) {
+  if (c->tp_block) {
+    REQ(c->tp_host.part_rows == max_tokens, "exchange already allocated with another capacity");
+    return FP_OK;
+  }
+  const size_t part = (size_t)max_tokens * c->cfg.hidden * 2;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMalloc(&c->tp_block, tp_header_bytes() + 2 * part));
+  CK(cudaMemset(c->tp_block, 0, tp_header_bytes()));
+  CK(cudaMalloc(&c->tp_local, sizeof(TpLocal)));
+  CK(cudaMemset(c->tp_local, 0, sizeof(TpLocal)));
+  c->tp_host.part_rows = max_tokens;
+  return FP_OK;
+}
+
+// bases[r] = rank r's exchange block as addressable from this context's device
+static int tp_finish(fp_ctx* c, char* const* bases) {
+  TpDev& d = c->tp_host;
+  d.rank = c->tp_rank;
+  d.size = c->tp_size;
+  d.local = c->tp_local;
+  const size_t part = (size_t)d.part_rows * c->cfg.hidden * 2;
+  for (int r = 0; r < c->tp_size; ++r) {
+    d.peer[r] = reinterpret_cast<TpShared*>(bases[r]);
+    for (int b = 0; b < 2; ++b)
+      d.part[r][b] = reinterpret_cast<__nv_bfloat16*>(bases[r] + tp_header_bytes() + b * part);
+  }
+  CK(cudaSetDevice(c->device));
+  if (!c->d_tp) CK(cudaMalloc(&c->d_tp, sizeof(TpDev)));
+  CK(cudaMemcpy(c->d_tp, &d, sizeof(TpDev), cudaMemcpyHostToDevice));
+  c->tp_connected = true;
+  return FP_OK;
+}
+
+int fp_tp_export(fp_ctx* c, int64_t max_tokens, fp_tp_handle* out) {
+  REQ(c && out, "null argument");
+  REQ(c->tp_size > 1, "context is not tensor parallel");
+  REQ(max_tokens >= 1, "max_tokens must be >= 1");
+  int rc = tp_alloc_block(c, max_tokens);
+  if (rc) return rc;
+  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(out->ipc), "ipc handle size");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->tp_block));
+  memset(out, 0, sizeof(*out));
+  memcpy(out->ipc, &h, sizeof(h));
+  out->part_rows = max_tokens;
+  out->rank = c->tp_rank;
+  out->device = c->device;
+  return FP_OK;
+}
+
+int fp_tp_import(fp_ctx* c, const fp_tp_handle* all) {
+  REQ(c && all, "null argument");
+  REQ(c->tp_block, "call fp_tp_export first");
+  REQ(!c->tp_connected, "already connected");
+  CK(cudaSetDevice(c->device));
+  std::vector<char*> bases(c->tp_size);
+  for (int r = 0; r < c->tp_size; ++r) {
+    REQ(all[r].rank == r, "handles must be ordered by rank");
+    REQ(all[r].part_rows == c->tp_host.part_rows, "ranks disagree on the exchange capacity");
+    if (r == c->tp_rank) {
+      bases[r] = c->tp_block;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, all[r].ipc, sizeof(h));
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    c->tp_opened.push_back(ptr);
+    bases[r] = static_cast<char*>(ptr);
+  }
+  return tp_finish(c, bases.data());
+}
+
+int fp_tp_connect_local(fp_ctx** ctxs, int32_t n, int64_t max_tokens) {
+  REQ(ctxs && n >= 2 && n <= kTpMax, "need 2..8 contexts");
+  REQ(max_tokens >= 1, "max_tokens must be >= 1");
+  bool same_device = true;
+  for (int r = 0; r < n; ++r) {
+    REQ(ctxs[r] && ctxs[r]->tp_size == n && ctxs[r]->tp_rank == r,
+        "contexts must be ranks 0..n-1 of a tp_size == n group, in order");
+    REQ(!ctxs[r]->tp_connected, "already connected");
+    same_device = same_device && ctxs[r]->device == ctxs[0]->device;
+  }
+  std::vector<char*> bases(n);
+  for (int r = 0; r < n; ++r) {
+    int rc = tp_alloc_block(ctxs[r], max_tokens);
+    if (rc) return rc;
+    bases[r] = ctxs[r]->tp_block;
+  }
+  if (!same_device) {
+    for (int a = 0; a < n; ++a) {
+      CK(cudaSetDevice(ctxs[a]->device));
+      for (int b = 0; b < n; ++b) {
+        if (ctxs[b]->device == ctxs[a]->device) continue;
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, ctxs[a]->device, ctxs[b]->device));
+        REQ(ok, "devices without peer access");
+        cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[b]->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CK(e);
+      }
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    int rc = tp_finish(ctxs[r], bases.data());
+    if (rc) return rc;
+    if (same_device) {  // one device: every rank's kernels go to rank 0's stream, in lock step
+      ctxs[r]->stream = ctxs[0]->own_stream;
+      ctxs[r]->tp_lockstep = true;
+    }
+  }
+  return FP_OK;
+}
+
+int fp_tp_enqueue_lockstep(fp_ctx** ctxs, fp_task** tasks, int32_t n, int32_t first,
+                           int32_t last) {
+  REQ(ctxs && tasks && n >= 2, "null argument");
+  std::vector<Task*> ts(n);
+  for (int r = 0; r < n; ++r) {
+    REQ(ctxs[r] && ctxs[r]->tp_lockstep && ctxs[r]->tp_rank == r && ctxs[r]->tp_size == n,
+        "contexts must form a lock-step group (fp_tp_connect_local on one device)");
+    ts[r] = reinterpret_cast<Task*>(tasks[r]);
+    REQ(ts[r] && ts[r]->n_entries == ts[0]->n_entries, "tasks must have identical timelines");
+    REQ(first >= ts[r]->seg_first && first <= last && last <= ts[r]->n_entries, "bad entry range");
+  }
+  CK(cudaSetDevice(ctxs[0]->device));
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int r = 0; r < n; ++r) locks.emplace_back(ctxs[r]->launch_mu);
+  for (int e = first; e < last; ++e)
+    for (int phase : {kPhasePre, kPhasePost})
+      for (int r = 0; r < n; ++r) {  // rank 0 first: its boundary decision precedes the others'
+        int rc = launch_entry(ctxs[r], ts[r], e, phase);
+        if (rc) return rc;
+      }
+  for (int r = 0; r < n; ++r) {
+    ts[r]->enq = std::max(ts[r]->enq, (int)last);
+    if (last == ts[r]->n_entries) {
+      CK(cudaEventRecord(ts[r]->done, ctxs[r]->stream));
+      ts[r]->done_recorded = 1;
+    }
+  }
+  CK(cudaGetLastError());
+  return FP_OK;
+}
+
+int fp_ctx_tp_counters(fp_ctx* c, int32_t* out4) {
+  REQ(c && out4, "null argument");
+  if (!c->tp_local) {
+    memset(out4, 0, 16);
+    return FP_OK;
+  }
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  TpLocal l;
+  CK(cudaMemcpy(&l, c->tp_local, sizeof(l), cudaMemcpyDeviceToHost));
+  out4[0] = l.xcount;
+  out4[1] = l.bcount;
+  out4[2] = l.gemm_ctr;
+  out4[3] = l.ar_ctr;
   return FP_OK;
 }
 

@@ -39,6 +39,7 @@ from prefillsim.engine import (  # noqa: E402
     ExecutionTask,
     SchedulerInvariantError,
     TaskState,
+    tp_sync_check,
 )
 
 _BOUNDARY = _ref_engine._BOUNDARY
@@ -141,6 +142,14 @@ class GpuEngine(Engine):
             ctx.signal()
             task.native.enqueue(nxt, nxt + 1)
             ctx.sync()
+            if hasattr(task.native, "poll_all"):
+                # tensor parallel: every rank must have stopped at the same entry -- the
+                # reference's lane gate (tp_sync_check, engine.py:50-57,254-255) over the
+                # device cursors of all ranks
+                lanes = task.native.poll_all()
+                if not tp_sync_check([s.cursor for s in lanes]):
+                    raise SchedulerInvariantError(
+                        f"TP ranks stopped at different entries: {[s.cursor for s in lanes]}")
             st = task.native.poll()
             self.binding.handshakes.append((task.task_id, nxt, st.cursor, st.state))
             if st.state != _lib.FP_TASK_STOPPED or st.cursor != nxt:

@@ -61,10 +61,13 @@ class PrefillContext:
         page_size: int = 128,
         max_pos: int = 65536,
         window: int = 8,
+        tp_rank: int = 0,
+        tp_size: int = 1,
     ):
         self.lib = _lib.load()
         self.shape = shape
         self.page_size = page_size
+        self.tp_rank, self.tp_size = tp_rank, tp_size
         cfg = _lib.ModelCfg(
             shape.num_layers,
             shape.hidden,
@@ -81,8 +84,8 @@ class PrefillContext:
         )
         h = C.c_void_p()
         _lib.check(
-            self.lib.fp_ctx_create(device, C.byref(cfg), 0, 1, None, kv_pages, page_size,
-                                   C.byref(h)),
+            self.lib.fp_ctx_create(device, C.byref(cfg), tp_rank, tp_size, None, kv_pages,
+                                   page_size, C.byref(h)),
             "fp_ctx_create",
         )
         self.h = h
@@ -163,6 +166,25 @@ class PrefillContext:
                         "flops": r.flops, "bytes": r.bytes, "ms": r.ms})
         return out
 
+    # -- tensor parallelism (one process per GPU) ---------------------------------------
+    def tp_export(self, max_tokens: int) -> bytes:
+        """This rank's exchange block handle (gather it from every rank, then tp_import)."""
+        hd = _lib.TpHandle()
+        _lib.check(self.lib.fp_tp_export(self.h, max_tokens, C.byref(hd)), "fp_tp_export")
+        return bytes(memoryview(hd))
+
+    def tp_import(self, handles: Sequence[bytes]) -> None:
+        arr = (_lib.TpHandle * len(handles))()
+        for i, b in enumerate(handles):
+            C.memmove(C.byref(arr[i]), b, C.sizeof(_lib.TpHandle))
+        _lib.check(self.lib.fp_tp_import(self.h, arr), "fp_tp_import")
+
+    def tp_counters(self) -> dict:
+        out = (C.c_int32 * 4)()
+        _lib.check(self.lib.fp_ctx_tp_counters(self.h, out), "fp_ctx_tp_counters")
+        return {"exchanges": out[0], "boundaries": out[1], "gemm_ticket": out[2],
+                "allreduce_ticket": out[3]}
+
     def launch_count(self) -> int:
         n = C.c_int64()
         _lib.check(self.lib.fp_ctx_launch_count(self.h, C.byref(n)), "fp_ctx_launch_count")
@@ -242,7 +264,7 @@ class PrefillTask:
     def read_kv(self, seq: int, layer: int) -> tuple[np.ndarray, np.ndarray]:
         sh = self.ctx.shape
         n = self.lens[seq]
-        k = np.empty((n, sh.n_kv_heads, sh.head_dim), np.uint16)
+        k = np.empty((n, sh.n_kv_heads // self.ctx.tp_size, sh.head_dim), np.uint16)
         v = np.empty_like(k)
         _lib.check(
             self.lib.fp_task_read_kv(self.ctx.h, self.h, seq, layer, k.ctypes.data, v.ctypes.data),
@@ -254,3 +276,146 @@ class PrefillTask:
         if self.h is not None:
             _lib.check(self.lib.fp_task_destroy(self.ctx.h, self.h), "fp_task_destroy")
             self.h = None
+
+
+def connect_tp_dist(ctx: PrefillContext, max_tokens: int, group=None) -> None:
+    """One process per GPU: exchange the ranks' block handles over torch.distributed (any
+    backend; the handles are 88-byte host objects) and map every peer's block."""
+    import torch.distributed as dist
+
+    mine = ctx.tp_export(max_tokens)
+    handles: list = [None] * ctx.tp_size
+    dist.all_gather_object(handles, mine, group=group)
+    ctx.tp_import(handles)
+
+
+class TPGroup:
+    """A tensor-parallel group driven from one process.
+
+    Each rank is a ``PrefillContext`` holding its Megatron shard. On one device the ranks share
+    rank 0's stream and run in lock step (``fp_tp_enqueue_lockstep``); the device code -- the
+    exchange GEMM, the peer-memory all-reduce, the rank-0 boundary decision ring -- is the same
+    code a one-process-per-GPU deployment runs (``connect_tp_dist``). The group exposes the
+    ``PrefillContext`` surface the engines use, so ``GpuEngine`` drives it unchanged.
+    """
+
+    def __init__(self, shape: ModelShape, tp: int, device=0, kv_pages: int = 256,
+                 page_size: int = 128, max_pos: int = 65536, max_tokens: int = 8192):
+        devices = list(device) if isinstance(device, (list, tuple)) else [device] * tp
+        self.shape = shape
+        self.tp_size = tp
+        self.page_size = page_size
+        self.max_tokens = max_tokens
+        self.ranks = [PrefillContext(shape, devices[r], kv_pages, page_size, max_pos,
+                                     tp_rank=r, tp_size=tp) for r in range(tp)]
+        self.lib = self.ranks[0].lib
+        arr = (C.c_void_p * tp)(*[c.h.value for c in self.ranks])
+        _lib.check(self.lib.fp_tp_connect_local(arr, tp, max_tokens), "fp_tp_connect_local")
+        self.stream_ptr = self.ranks[0].stream_ptr
+
+    def init_random(self, seed: int, std: float = 0.02) -> None:
+        for c in self.ranks:
+            c.init_random(seed, std)
+
+    def load_weights(self, w: dict) -> None:
+        for c in self.ranks:  # full tensors; every rank keeps its shard
+            c.load_weights(w)
+
+    def create_task(self, tokens, chunk_tokens=None, granularity="operator",
+                    task_id: int = 0) -> "TPTask":
+        return TPTask(self, tokens, chunk_tokens, granularity, task_id)
+
+    def signal(self) -> None:
+        self.ranks[0].signal()  # only rank 0's device reads the flag
+
+    def clear(self) -> None:
+        for c in self.ranks:
+            c.clear()
+
+    def poll(self) -> _lib.Status:
+        return self.ranks[0].poll()
+
+    def sync(self) -> None:
+        for c in self.ranks:
+            c.sync()
+
+    def free_pages(self) -> int:
+        return min(c.free_pages() for c in self.ranks)
+
+    def profile(self, on: bool) -> None:
+        for c in self.ranks:
+            c.profile(on)
+
+    def drain_profile(self, max_records: int = 1 << 20) -> list[dict]:
+        out = []
+        for r, c in enumerate(self.ranks):
+            for rec in c.drain_profile(max_records):
+                rec["rank"] = r
+                out.append(rec)
+        return out
+
+    def launch_count(self) -> int:
+        return sum(c.launch_count() for c in self.ranks)
+
+    def tp_counters(self) -> list[dict]:
+        return [c.tp_counters() for c in self.ranks]
+
+    def close(self) -> None:
+        for c in reversed(self.ranks):  # followers first: they use rank 0's stream
+            c.close()
+
+
+class TPTask:
+    """One prefill task replicated over the ranks of a ``TPGroup`` (identical entry lists)."""
+
+    def __init__(self, group: TPGroup, tokens, chunk_tokens, granularity, task_id):
+        self.group = group
+        self.ctx = group
+        self.lib = group.lib
+        self.task_id = task_id
+        self.parts = [c.create_task(tokens, chunk_tokens, granularity, task_id)
+                      for c in group.ranks]
+        self.lens = self.parts[0].lens
+        self.n_entries = self.parts[0].n_entries
+
+    def info(self) -> dict:
+        return self.parts[0].info()
+
+    def entry_info(self, i: int):
+        return self.parts[0].entry_info(i)
+
+    def begin_segment(self, first: int) -> None:
+        for t in self.parts:
+            t.begin_segment(first)
+
+    def enqueue(self, first: int, last: int) -> None:
+        n = self.group.tp_size
+        ctxs = (C.c_void_p * n)(*[c.h.value for c in self.group.ranks])
+        tasks = (C.c_void_p * n)(*[t.h.value for t in self.parts])
+        _lib.check(self.lib.fp_tp_enqueue_lockstep(ctxs, tasks, n, first, last),
+                   "fp_tp_enqueue_lockstep")
+
+    def poll_all(self) -> list:
+        return [t.poll() for t in self.parts]
+
+    def poll(self) -> _lib.TaskStatus:
+        sts = self.poll_all()
+        if len({(s.state, s.cursor) for s in sts}) != 1:
+            raise _lib.NativeError(
+                "tensor-parallel ranks diverged: "
+                + ", ".join(f"rank {r}: state {s.state} cursor {s.cursor}" for r, s in enumerate(sts)))
+        return sts[0]
+
+    def logits(self) -> np.ndarray:
+        return self.parts[0].logits()  # lm_head is replicated; every rank holds the same logits
+
+    def rank_logits(self) -> list:
+        return [t.logits() for t in self.parts]
+
+    def read_kv(self, seq: int, layer: int) -> tuple[np.ndarray, np.ndarray]:
+        ks, vs = zip(*(t.read_kv(seq, layer) for t in self.parts))
+        return np.concatenate(ks, axis=1), np.concatenate(vs, axis=1)  # heads are rank-major
+
+    def destroy(self) -> None:
+        for t in reversed(self.parts):
+            t.destroy()

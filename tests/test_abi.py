@@ -59,5 +59,9 @@ def test_argument_validation(lib):
     assert lib.fp_ctx_create(0, C.byref(cfg), 0, 1, None, 8, 128, C.byref(h)) == -1
     assert b"head_dim" in lib.fp_last_error()
     cfg.head_dim = 128
-    assert lib.fp_ctx_create(0, C.byref(cfg), 0, 2, None, 8, 128, C.byref(h)) == -1
+    assert lib.fp_ctx_create(0, C.byref(cfg), 0, 3, None, 8, 128, C.byref(h)) == -1  # 2 kv heads
+    assert b"tp_size" in lib.fp_last_error()
+    assert lib.fp_ctx_create(0, C.byref(cfg), 2, 2, None, 8, 128, C.byref(h)) == -1  # rank >= size
+    assert lib.fp_ctx_create(0, C.byref(cfg), 0, 2, C.c_void_p(1), 8, 128, C.byref(h)) == -1
+    assert b"nccl_comm" in lib.fp_last_error()
     assert lib.fp_ctx_create(0, C.byref(cfg), 0, 1, None, 8, 64, C.byref(h)) == -1
