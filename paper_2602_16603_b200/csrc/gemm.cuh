@@ -56,7 +56,17 @@ struct GemmParams {
   float* ws;
   int* tickets;
   int xchg;  // tensor parallel o_proj/down_proj: store the partial sum into this rank's exchange
-  int pad3;  // buffer (EPI_STORE_BF16) and publish it to the peers (tp_publish_partial)
+             // buffer (EPI_STORE_BF16) and publish it to the peers (tp_publish_partial)
+  // Fused RMSNorm. The norm weight is folded into the weight columns (W' = W diag(gamma)), so
+  // rmsnorm(h) W^T = rsqrt(mean(h^2) + eps) * (h W'^T): the GEMM reads the residual stream h
+  // directly and the EPI_QKV / EPI_SWIGLU epilogue scales its row by the rsqrt factor, built
+  // from `ssq_in` = per-row sums of squares of h in 256-column segments [M, nseg] (summed in
+  // segment order: deterministic). EPI_RESID writes those segment sums of the new h into
+  // `ssq_out` (tile n-block nb = segment nb) for the next norm.
+  int nseg;
+  float norm_eps_in;  // eps of the fused input RMSNorm
+  const float* ssq_in;
+  float* ssq_out;
   Guard guard;
 };
 
@@ -321,13 +331,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       // Accumulator columns [col, col+32) of this thread's row: from TMEM, or the in-order sum
       // of the split partials (split 0 first) -- the same bits whichever CTA arrives last.
+      // fused RMSNorm: the row's rsqrt factor (1 for epilogues without a norm in front)
+      float rs = 1.f;
+      if ((EPI == EPI_QKV || EPI == EPI_SWIGLU) && p.ssq_in != nullptr && live) {
+        const float* sp = p.ssq_in + (long long)m * p.nseg;
+        float ssum = 0.f;
+        for (int i = 0; i < p.nseg; ++i) ssum += __ldg(sp + i);
+        rs = rsqrtf(ssum / (float)(p.nseg * 256) + p.norm_eps_in);
+      }
       auto load32 = [&](int col, float* v) {
         if (splits == 1) {
           uint32_t r[32];
           tmem_ld32(tacc + col, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * rs;
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -342,6 +360,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               v[4 * i + 3] += f.w;
             }
           }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= rs;
         }
       };
 
@@ -357,6 +377,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&tfull[acc], acc_ph);
           tc_fence_after();
         }
+        float ss = 0.f;
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
           float v[32];
@@ -373,9 +394,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 v[8 * i + 2 * j + 1] += f.y;
               }
             }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {  // the next norm sees the bf16-rounded values
+              const float rv = __bfloat162float(__float2bfloat16(v[i]));
+              ss += rv * rv;
+            }
             store_row32_bf16(hrow + c * 32, v);
           }
         }
+        if (live && p.ssq_out) p.ssq_out[(long long)m * p.nseg + nb] = ss;
       } else if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32) {
         void* out = p.out;
         if (EPI == EPI_STORE_BF16 && p.xchg) {

@@ -18,10 +18,12 @@ struct RmsParams {
   __nv_bfloat16* h_out;  // with ids: the residual stream is initialised with the embedding row
   long long ld_h;
   const __nv_bfloat16* gamma;  // [d]
-  __nv_bfloat16* out;  // [M, ld_out]
+  __nv_bfloat16* out;  // [M, ld_out]; null: only the embedding copy + segment sums
   long long ld_out;
   float eps;
-  int pad;
+  int nseg;            // with ssq: d / 256
+  float* ssq;          // optional [M, nseg]: sums of squares per 256-column segment (the
+                       // fused-norm input of the next GEMM, see GemmParams::ssq_in)
   Guard guard;
 };
 
@@ -50,7 +52,10 @@ __global__ void __launch_bounds__(1024) rmsnorm_kernel(const RmsParams p) {
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0) red[warp] = ss;
+  if (lane == 0) red[warp] = ss;  // one warp = one 256-column segment
+  if (p.ssq && lane == 0) p.ssq[(long long)row * p.nseg + warp] = ss;
+  if (p.ids && p.h_out) st_global_v4(p.h_out + (long long)row * p.ld_h + c, raw);
+  if (p.out == nullptr) return;
   __syncthreads();
   if (warp == 0) {
     const int nw = blockDim.x >> 5;
@@ -61,7 +66,6 @@ __global__ void __launch_bounds__(1024) rmsnorm_kernel(const RmsParams p) {
   }
   __syncthreads();
   const float r = rsqrtf(red[0] / (float)p.d + p.eps);
-  if (p.ids && p.h_out) st_global_v4(p.h_out + (long long)row * p.ld_h + c, raw);
   const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
   uint32_t o[4];
 #pragma unroll

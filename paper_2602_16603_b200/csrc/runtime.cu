@@ -94,8 +94,28 @@ __global__ void init_normal_kernel(__nv_bfloat16* w, long long n, uint64_t seed,
   }
 }
 
+// RMSNorm weight folding (fused norm, see GemmParams::ssq_in): W[row, k] *= g_new[k] / g_old[k]
+// over rows row0 + b * bstride + j (b < nblocks, j < rpb); g_old == null: divide by 1.
+__global__ void fold_cols_kernel(__nv_bfloat16* w, long long row0, int nblocks, long long bstride,
+                                 int rpb, int d, const __nv_bfloat16* g_new,
+                                 const __nv_bfloat16* g_old) {
+  const long long n = (long long)nblocks * rpb * d;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / d;
+    const int k = (int)(i - r * d);
+    const long long row = row0 + (r / rpb) * bstride + r % rpb;
+    float f = __bfloat162float(g_new[k]);
+    if (g_old) f /= __bfloat162float(g_old[k]);
+    __nv_bfloat16* e = w + row * d + k;
+    *e = __float2bfloat16(__bfloat162float(*e) * f);
+  }
+}
+
 // --------------------------------------------------------------------------- structures
 struct Layer {
+  // wqkv / wgu hold the norm weights folded into their columns; attn_g / ffn_g are the gammas
+  // currently folded in (bf16, as loaded; all ones before any load)
   __nv_bfloat16 *wqkv, *wo, *wgu, *wd, *attn_g, *ffn_g;
   float* bqkv = nullptr;                           // [qkv_n] (qkv_bias models)
   float *q_norm = nullptr, *k_norm = nullptr;      // [128]  (qk_norm models)
@@ -122,10 +142,11 @@ struct Task {
   char* meta = nullptr;  // one allocation: ids | pos | tok_page | items | bt | last_rows
   int *d_ids, *d_pos, *d_tpage, *d_bt, *d_last;
   AttnTile* d_items;
-  __nv_bfloat16 *h, *xn, *q, *ao, *act, *xf;
+  __nv_bfloat16 *h, *q, *ao, *act, *xf;
+  float* ssq;  // [max_m, hidden/256] segment sums of squares of h (fused RMSNorm input)
   float* logits;
   TaskCtl* ctl;
-  CUtensorMap tm_xn, tm_ao, tm_act, tm_xf, tm_q;
+  CUtensorMap tm_h, tm_ao, tm_act, tm_xf, tm_q;
   cudaEvent_t ready, done;
   // host execution state
   int gen = 0, seg_first = 0, enq = 0, seg_ack0 = 0, done_recorded = 0;
@@ -411,32 +432,37 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
 
   const bool xchg_op = c->tp_size > 1 && (op == FP_OP_O_PROJ || op == FP_OP_DOWN_PROJ);
   if (!xchg_op && !(phase & kPhasePre)) return FP_OK;  // single-phase entries run in phase 1
+  const int nseg = m.hidden / 256;
   if (op == FP_OP_QKV_PROJ || op == FP_OP_GATE_UP_PROJ) {
-    RmsParams r{};
-    r.M = M;
-    r.d = m.hidden;
-    r.src = t->h;
-    r.ld_src = m.hidden;
-    if (op == FP_OP_QKV_PROJ && layer == 0) {  // chunk start: embedding gather into h
+    // The input RMSNorm is fused: the GEMM reads h with the norm weight folded into its weight
+    // columns and scales rows by rsqrt(mean(h^2) + eps) from the segment sums in t->ssq.
+    Guard gg = g;
+    if (op == FP_OP_QKV_PROJ && layer == 0) {  // chunk start: embedding gather into h (+ sums)
+      RmsParams r{};
+      r.M = M;
+      r.d = m.hidden;
       r.src = c->embed;
+      r.ld_src = m.hidden;
       r.ids = ids;
       r.h_out = t->h;
       r.ld_h = m.hidden;
-    }
-    r.gamma = op == FP_OP_QKV_PROJ ? ly.attn_g : ly.ffn_g;
-    r.out = t->xn;
-    r.ld_out = m.hidden;
-    r.eps = m.rms_eps;
-    r.guard = g;
-    {
-      ProfScope ps(c, st, FP_K_RMS, layer, M, 0.0, (layer == 0 && op == 0 ? 3.0 : 2.0) * M * m.hidden * 2);
+      r.gamma = ly.attn_g;
+      r.eps = m.rms_eps;
+      r.nseg = nseg;
+      r.ssq = t->ssq;
+      r.guard = g;
+      ProfScope ps(c, st, FP_K_RMS, layer, M, 0.0, 2.0 * M * m.hidden * 2);
       int rc = launch_rms(r, st);
       if (rc) return rc;
+      gg = g2;
     }
     GemmParams p{};
     p.M = M;
     p.K = m.hidden;
-    p.guard = g2;
+    p.guard = gg;
+    p.nseg = nseg;
+    p.ssq_in = t->ssq;
+    p.norm_eps_in = m.rms_eps;
     if (op == FP_OP_QKV_PROJ) {
       p.N = c->qkv_n;
       p.pos = pos;
@@ -454,13 +480,13 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
       p.k_norm = ly.k_norm;
       p.norm_eps = m.rms_eps;
       ProfScope ps(c, st, FP_K_QKV, layer, M, 2.0 * M * p.N * p.K, 0.0);
-      launch_gemm<EPI_QKV>(c, t->tm_xn, ly.tm_qkv, p, st);
+      launch_gemm<EPI_QKV>(c, t->tm_h, ly.tm_qkv, p, st);
     } else {
       p.N = 2 * c->ffn;
       p.out = t->act;
       p.ldo = c->ffn;
       ProfScope ps(c, st, FP_K_GATE_UP, layer, M, 2.0 * M * p.N * p.K, 0.0);
-      launch_gemm<EPI_SWIGLU>(c, t->tm_xn, ly.tm_gu, p, st);
+      launch_gemm<EPI_SWIGLU>(c, t->tm_h, ly.tm_gu, p, st);
     }
   } else if (op == FP_OP_ATTN) {
     AttnTcParams a{};
@@ -488,6 +514,8 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
     p.resid = t->h;
     p.ldr = m.hidden;
     p.guard = g;
+    p.nseg = nseg;
+    p.ssq_out = t->ssq;  // segment sums of the new h for the next fused norm
     p.K = op == FP_OP_O_PROJ ? c->qdim : c->ffn;
     const CUtensorMap& ta = op == FP_OP_O_PROJ ? t->tm_ao : t->tm_act;
     const CUtensorMap& tb = op == FP_OP_O_PROJ ? ly.tm_o : ly.tm_d;
@@ -508,6 +536,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
       x.d = m.hidden;
       x.h = t->h;
       x.ldh = m.hidden;
+      x.ssq = t->ssq;
       x.guard = g2;
       const long long vecs = (long long)M * m.hidden / 8;
       const int grid = (int)std::max(1LL, std::min<long long>((vecs + 255) / 256, 8LL * c->num_sms));
@@ -642,6 +671,11 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     CK(cudaMalloc(&ly.wd, (size_t)d * c->ffn * 2));
     CK(cudaMalloc(&ly.attn_g, (size_t)d * 2));
     CK(cudaMalloc(&ly.ffn_g, (size_t)d * 2));
+    {
+      const std::vector<uint16_t> ones(d, 0x3F80);  // bf16 1.0: nothing folded yet
+      CK(cudaMemcpy(ly.attn_g, ones.data(), (size_t)d * 2, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ly.ffn_g, ones.data(), (size_t)d * 2, cudaMemcpyHostToDevice));
+    }
     if (cfg->qkv_bias) {
       CK(cudaMalloc(&ly.bqkv, (size_t)c->qkv_n * 4));
       CK(cudaMemset(ly.bqkv, 0, (size_t)c->qkv_n * 4));
@@ -784,6 +818,14 @@ static int load_f32_vec(float* dst, const void* host, int64_t n) {
   return FP_OK;
 }
 
+static void fold(fp_ctx* c, __nv_bfloat16* w, long long row0, int nblocks, long long bstride,
+                 int rpb, const __nv_bfloat16* g_new, const __nv_bfloat16* g_old) {
+  const long long n = (long long)nblocks * rpb * c->cfg.hidden;
+  const int grid = (int)std::min<long long>((n + 255) / 256, 16LL * c->num_sms);
+  fold_cols_kernel<<<grid, 256, 0, c->stream>>>(w, row0, nblocks, bstride, rpb, c->cfg.hidden,
+                                                g_new, g_old);
+}
+
 int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, int64_t n) {
   REQ(c && host, "null argument");
   CK(cudaSetDevice(c->device));
@@ -818,6 +860,8 @@ int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, 
       const long long off = q ? 0 : (tensor == FP_W_K ? c->qdim : c->qdim + c->kvdim);
       CK(cudaMemcpy(ly.wqkv + off * d, src + r * rows * d * 2, (size_t)rows * d * 2,
                     cudaMemcpyHostToDevice));
+      fold(c, ly.wqkv, off, 1, 0, (int)rows, ly.attn_g, nullptr);  // fused input norm
+      CK(cudaStreamSynchronize(c->stream));
       return FP_OK;
     }
     case FP_W_O:
@@ -840,14 +884,34 @@ int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, 
       for (int b = 0; b < c->ffn / 128; ++b)
         CK(cudaMemcpy(ly.wgu + ((size_t)b * 256 + half * 128) * d, base + (size_t)b * 128 * d * 2,
                       (size_t)128 * d * 2, cudaMemcpyHostToDevice));
+      fold(c, ly.wgu, half * 128, c->ffn / 128, 256, 128, ly.ffn_g, nullptr);
+      CK(cudaStreamSynchronize(c->stream));
       return FP_OK;
     }
     case FP_W_ATTN_NORM:
-    case FP_W_FFN_NORM:
+    case FP_W_FFN_NORM: {
+      // re-fold the projection columns from the gamma folded so far to the new one (load
+      // norms before projections to fold with a single rounding)
       REQ(n == d, "weight size mismatch");
-      CK(cudaMemcpy(tensor == FP_W_ATTN_NORM ? ly.attn_g : ly.ffn_g, host, (size_t)n * 2,
-                    cudaMemcpyHostToDevice));
+      const bool attn = tensor == FP_W_ATTN_NORM;
+      __nv_bfloat16* g = attn ? ly.attn_g : ly.ffn_g;
+      std::vector<uint16_t> old(d);
+      CK(cudaMemcpy(old.data(), g, (size_t)d * 2, cudaMemcpyDeviceToHost));
+      const uint16_t* nw = static_cast<const uint16_t*>(host);
+      for (long long k = 0; k < d; ++k)
+        if ((old[k] & 0x7FFF) == 0 && nw[k] != old[k])
+          return set_err(FP_ERR_STATE, "a zero norm weight was folded into the projection; "
+                                       "reload the projection weights after this norm");
+      __nv_bfloat16* gnew = nullptr;
+      CK(cudaMalloc(&gnew, (size_t)d * 2));
+      CK(cudaMemcpy(gnew, host, (size_t)d * 2, cudaMemcpyHostToDevice));
+      if (attn) fold(c, ly.wqkv, 0, 1, 0, c->qdim + 2 * c->kvdim, gnew, g);
+      else fold(c, ly.wgu, 0, 1, 0, 2 * c->ffn, gnew, g);
+      CK(cudaMemcpyAsync(g, gnew, (size_t)d * 2, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      cudaFree(gnew);
       return FP_OK;
+    }
     case FP_W_Q_BIAS:
     case FP_W_K_BIAS:
     case FP_W_V_BIAS: {
@@ -888,6 +952,8 @@ int fp_weights_init_random(fp_ctx* c, uint64_t seed, float stdv) {
     fill(ly.wd, d * c->ffn, 0.f, stdv, true);
     fill(ly.attn_g, d, 1.f, 0.1f);
     fill(ly.ffn_g, d, 1.f, 0.1f);
+    fold(c, ly.wqkv, 0, 1, 0, c->qdim + 2 * c->kvdim, ly.attn_g, nullptr);  // fused norms
+    fold(c, ly.wgu, 0, 1, 0, 2 * c->ffn, ly.ffn_g, nullptr);
     if (ly.bqkv || ly.q_norm) {
       std::vector<float> v(c->qkv_n, 0.f);
       for (int i = 0; i < c->qdim + 2 * c->kvdim; ++i) v[i] = 0.02f * (float)((int)((s * 2654435761ull + i * 40503ull) % 2001) - 1000) / 1000.f;
@@ -1070,7 +1136,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   // workspaces (resume state lives here: h + the live intermediate)
   const long long M = t->max_m, d = m.hidden;
   CK(cudaMallocAsync((void**)&t->h, M * d * 2, up));
-  CK(cudaMallocAsync((void**)&t->xn, M * d * 2, up));
+  CK(cudaMallocAsync((void**)&t->ssq, M * (d / 256) * 4, up));
   CK(cudaMallocAsync((void**)&t->q, M * c->qdim * 2, up));
   CK(cudaMallocAsync((void**)&t->ao, M * c->qdim * 2, up));
   CK(cudaMallocAsync((void**)&t->act, M * (long long)c->ffn * 2, up));
@@ -1082,7 +1148,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   CK(cudaMemsetAsync(t->ctl, 0, ctl_bytes, up));
   CK(cudaMemsetAsync(&t->ctl->stopped_gen, 0xFF, 4, up));  // -1
   int rc;
-  if ((rc = make_map(&t->tm_xn, t->xn, M, d, 128))) return rc;
+  if ((rc = make_map(&t->tm_h, t->h, M, d, 128))) return rc;
   if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
   if ((rc = make_map(&t->tm_act, t->act, M, c->ffn, 128))) return rc;
   if ((rc = make_map(&t->tm_xf, t->xf, n_seqs, d, 128))) return rc;
@@ -1136,7 +1202,7 @@ int fp_task_destroy(fp_ctx* c, fp_task* task) {
     cudaStreamWaitEvent(st, t->ready, 0);
     cudaFreeAsync(t->meta, st);
     cudaFreeAsync(t->h, st);
-    cudaFreeAsync(t->xn, st);
+    cudaFreeAsync(t->ssq, st);
     cudaFreeAsync(t->q, st);
     cudaFreeAsync(t->ao, st);
     cudaFreeAsync(t->act, st);

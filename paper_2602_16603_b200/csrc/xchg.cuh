@@ -24,9 +24,12 @@ struct XchgParams {
   int M, d;
   __nv_bfloat16* h;  // residual stream [M, ldh] (replicated on every rank)
   long long ldh;
+  float* ssq;        // [M, d/256] segment sums of squares of the new h (fused next RMSNorm)
   Guard guard;       // guard.tp carries the peer pointers
 };
 
+// One warp per (row, 256-column segment): 32 lanes x 8 bf16 = the segment, so the fused
+// norm's segment sum of squares is one warp reduction.
 __global__ void __launch_bounds__(256) tp_allreduce_kernel(const XchgParams p) {
   __shared__ int s_xc;
   grid_dep_wait();
@@ -42,11 +45,15 @@ __global__ void __launch_bounds__(256) tp_allreduce_kernel(const XchgParams p) {
   const int xc = s_xc;
   const int buf = xc & 1;
   const int n = tp->size;
-  const long long vpr = p.d / 8;  // 16-byte vectors per row
-  const long long total = (long long)p.M * vpr;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long m = i / vpr, c = (i - m * vpr) * 8;
+  const int lane = threadIdx.x & 31;
+  const int nseg = p.d / 256;
+  const long long units = (long long)p.M * nseg;
+  const long long wstep = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long u = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units;
+       u += wstep) {
+    const long long m = u / nseg;
+    const int sg = (int)(u - m * nseg);
+    const long long c = (long long)sg * 256 + lane * 8;
     __nv_bfloat16* hp = p.h + m * p.ldh + c;
     uint4 v[kTpMax];
 #pragma unroll
@@ -75,8 +82,21 @@ __global__ void __launch_bounds__(256) tp_allreduce_kernel(const XchgParams p) {
         }
       }
     }
-    st_global_v4(hp, make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                                pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7])));
+    const uint4 o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                               pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+    st_global_v4(hp, o);
+    if (p.ssq) {
+      float ss = 0.f;
+      const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(w[j]);
+        ss += f.x * f.x + f.y * f.y;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      if (lane == 0) p.ssq[m * nseg + sg] = ss;
+    }
   }
   // the last CTA advances the exchange counter (read by the next exchange GEMM / all-reduce)
   __syncthreads();

@@ -32,7 +32,11 @@ def bf16_to_f32(bits: np.ndarray) -> np.ndarray:
     return (bits.astype(np.uint32) << 16).view(np.float32)
 
 
+# Norm weights first: the library folds them into the projection columns (fused RMSNorm), and
+# a norm loaded after its projection costs a second bf16 rounding of the folded weights.
 _WEIGHT_IDS = {
+    "attn_norm": _lib.W_ATTN_NORM,
+    "ffn_norm": _lib.W_FFN_NORM,
     "wq": _lib.W_Q,
     "wk": _lib.W_K,
     "wv": _lib.W_V,
@@ -40,8 +44,6 @@ _WEIGHT_IDS = {
     "w_gate": _lib.W_GATE,
     "w_up": _lib.W_UP,
     "w_down": _lib.W_DOWN,
-    "attn_norm": _lib.W_ATTN_NORM,
-    "ffn_norm": _lib.W_FFN_NORM,
     "bq": _lib.W_Q_BIAS,
     "bk": _lib.W_K_BIAS,
     "bv": _lib.W_V_BIAS,
