@@ -219,6 +219,15 @@ int fp_op_gemm(fp_ctx* ctx, int32_t epi, const void* A, const void* B, void* C, 
                int32_t N, int32_t K);
 int fp_op_rmsnorm(fp_ctx* ctx, const void* x, const void* gamma, void* out, int32_t M,
                   int32_t d, float eps);
+/* GEMM tiling override for experiments and split-K parity tests: pair = -1 auto, 0 single-CTA
+ * tiles, 1 CTA-pair tiles; splits = 0 auto, S >= 1 forces S K-slices on the partial-wave tiles
+ * (clamped so the split units fit one round of the persistent grid). */
+int fp_ctx_set_gemm_policy(fp_ctx* ctx, int32_t pair, int32_t splits);
+/* Diagnostics: with FP_GEMM_STAMPS=1 in the environment at fp_ctx_create, every fp_op_gemm
+ * launch records per-CTA phase stamps (%globaltimer ns, 16 slots per CTA: entry, prologue done,
+ * boundary check done, first TMA, first MMA, last accumulator commit, epilogue start, partial
+ * stored, split barrier passed, split items done, exit, teardown). Copies max_ctas x 16. */
+int fp_debug_gemm_stamps(fp_ctx* ctx, uint64_t* out, int32_t max_ctas);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,8 @@ from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_native", "libflowprefill.so")
+# A/B experiments only: another build of the library (symbols it lacks stay unbound)
+_AB_PATH = os.environ.get("FP_AB_LIB")
 
 FP_OK = 0
 FP_GRAN = {"operator": 0, "layer": 1, "chunk": 2, "none": 3}
@@ -114,6 +116,8 @@ _SIGS = {
     "fp_ctx_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "fp_ctx_free_pages": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "fp_ctx_set_window": (C.c_int, [_P, _I]),
+    "fp_ctx_set_gemm_policy": (C.c_int, [_P, _I, _I]),
+    "fp_debug_gemm_stamps": (C.c_int, [_P, _P, _I]),
     "fp_sync": (C.c_int, [_P]),
     "fp_weights_init_random": (C.c_int, [_P, C.c_uint64, C.c_float]),
     "fp_weights_load": (C.c_int, [_P, _I, _I, _P, C.c_int64]),
@@ -155,6 +159,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    if _AB_PATH:
+        path = _AB_PATH
     if not os.path.exists(path):
         raise NativeError(
             f"native library missing: {path}. Build it with "
@@ -162,6 +168,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         )
     lib = C.CDLL(path)
     for name, (res, args) in _SIGS.items():
+        if _AB_PATH and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *sources()]
+    extra = ["-DFP_GEMM_STAMPS"] if os.environ.get("FP_GEMM_STAMPS_BUILD") else []
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", *sources()]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = proc.stdout + proc.stderr
     with open(os.path.join(OUT_DIR, "build.log"), "w") as fh:

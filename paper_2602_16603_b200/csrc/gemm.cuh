@@ -54,7 +54,7 @@ struct GemmParams {
   int splits;
   int full_tiles;
   float* ws;
-  int* tickets;
+  int* tickets;     // [2][1024] per split tile slot: arrivals, done
   int xchg;  // tensor parallel o_proj/down_proj: store the partial sum into this rank's exchange
              // buffer (EPI_STORE_BF16) and publish it to the peers (tp_publish_partial)
   // Fused RMSNorm. The norm weight is folded into the weight columns (W' = W diag(gamma)), so
@@ -67,8 +67,22 @@ struct GemmParams {
   float norm_eps_in;  // eps of the fused input RMSNorm
   const float* ssq_in;
   float* ssq_out;
+  unsigned long long* dbg;  // phase stamps (%globaltimer ns) [cta][16] for diagnostics, or null
   Guard guard;
 };
+
+// Phase stamps are compiled in only for diagnostic builds (-DFP_GEMM_STAMPS): even an idle
+// stamp perturbs the register allocation of the epilogue warps.
+#ifdef FP_GEMM_STAMPS
+#define GEMM_STAMP(k)                                                                 \
+  do {                                                                                \
+    if (p.dbg) p.dbg[(blockIdx.x + blockIdx.y * gridDim.x) * 16 + (k)] = globaltimer(); \
+  } while (0)
+#else
+#define GEMM_STAMP(k) \
+  do {                \
+  } while (0)
+#endif
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;
@@ -115,7 +129,226 @@ DEVI void store_row32_bf16(__nv_bfloat16* dst, const float* v) {
   }
 }
 
-template <int BN, int EPI, int CG>
+// Inter-CTA barrier of the K-slice CTAs of one split tile (epilogue warps only): arrive, then
+// spin until `n` arrivals (acquire).
+DEVI void split_barrier(int* ctr, int n) {
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (threadIdx.x % 128 == 0) {
+    atomicAdd(ctr, 1);
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= n) break;
+      __nanosleep(32);
+    }
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+// Split-K tile reduction. A split tile's fp32 K-slice partials sit in the L2 workspace as
+// [split][col/4][row] float4. Its epilogue is cut into 8 items per row, each summing 32 partial
+// columns -- [colA, colA + 16) and [colB, colB + 16) -- over the K-slices in split order (the
+// same bits on every run), with 4 slices' loads in flight.
+struct GmemSum {
+  const float4* ws_tile;
+  int S;
+  DEVI void get(int r, int colA, int colB, float* v) const {
+    constexpr int ILP = 4;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    const float4* sa = ws_tile + (long long)(colA / 4) * kGemmBM + r;
+    const float4* sb = ws_tile + (long long)(colB / 4) * kGemmBM + r;
+    const long long sstride = 64LL * kGemmBM;  // 256 columns / 4 per K-slice
+    for (int s0 = 0; s0 < S; s0 += ILP) {
+      float4 f[ILP][8];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j)
+        if (s0 + j < S) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            f[j][i] = __ldcg(sa + (s0 + j) * sstride + i * kGemmBM);
+            f[j][4 + i] = __ldcg(sb + (s0 + j) * sstride + i * kGemmBM);
+          }
+        }
+#pragma unroll
+      for (int j = 0; j < ILP; ++j)
+        if (s0 + j < S) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            v[4 * i] += f[j][i].x;
+            v[4 * i + 1] += f[j][i].y;
+            v[4 * i + 2] += f[j][i].z;
+            v[4 * i + 3] += f[j][i].w;
+          }
+        }
+    }
+  }
+};
+
+DEVI void store16_bf16(__nv_bfloat16* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    uint4 u;
+    u.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+    u.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+    u.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+    u.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+    st_global_v4(dst + 8 * i, u);
+  }
+}
+
+// Epilogue item g (0..7) of tile row r (token row m) of a split tile; n0 / nb = the tile's first
+// column / n-block. Called by all 32 lanes of a warp (valid = false lanes only join shuffles);
+// the 8 items of a row are 8 consecutive lanes. Items:
+//   EPI_RESID / EPI_STORE_*  columns [32g, 32g + 32)
+//   EPI_SWIGLU               gate columns [16g, 16g + 16) and the matching up columns (+128)
+//   EPI_QKV                  head h = g / 4, quarter q = g % 4: head columns [16q, 16q + 16)
+//                            and their RoPE partners [64 + 16q, 64 + 16q + 16)
+// EPI_RESID writes the row's sum of squares (8 chunk sums in chunk order) to ssq_out; the Qwen3
+// q/k-norm sums a head's 4 items in quarter order.
+template <int EPI>
+__device__ __noinline__ void split_item_epilogue(const GemmParams& p, const GmemSum& sum,
+                                                 bool valid, int m, int r, int g, int n0,
+                                                 int nb) {
+  constexpr int BN = 256;
+  const int lane = threadIdx.x & 31;
+  float rs = 1.f;  // fused input RMSNorm factor of the row
+  if ((EPI == EPI_QKV || EPI == EPI_SWIGLU) && p.ssq_in != nullptr && valid) {
+    const float* sp = p.ssq_in + (long long)m * p.nseg;
+    float ssum = 0.f;
+    for (int i = 0; i < p.nseg; ++i) ssum += __ldg(sp + i);
+    rs = rsqrtf(ssum / (float)(p.nseg * 256) + p.norm_eps_in);
+  }
+  float v[32];
+  if constexpr (EPI == EPI_RESID) {
+    __nv_bfloat16* hrow = p.resid + (long long)m * p.ldr + n0 + g * 32;
+    uint4 hv[4];  // residual loads in flight with the partial loads
+    float ss = 0.f;
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hv[i] = ld_global_v4(hrow + 8 * i);
+      sum.get(r, g * 32, g * 32 + 16, v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t hw[4] = {hv[i].x, hv[i].y, hv[i].z, hv[i].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack_bf16x2(hw[j]);
+          v[8 * i + 2 * j] += f.x;
+          v[8 * i + 2 * j + 1] += f.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {  // the next norm sees the bf16-rounded values
+        const float rv = __bfloat162float(__float2bfloat16(v[i]));
+        ss += rv * rv;
+      }
+      store_row32_bf16(hrow, v);
+    }
+    float tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tot += __shfl_sync(0xffffffffu, ss, (lane & ~7) + j);
+    if (valid && g == 0 && p.ssq_out != nullptr) p.ssq_out[(long long)m * p.nseg + nb] = tot;
+  } else if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32) {
+    if (!valid) return;
+    sum.get(r, g * 32, g * 32 + 16, v);
+    if constexpr (EPI == EPI_STORE_F32) {
+      float* dst = reinterpret_cast<float*>(p.out) + (long long)m * p.ldo + n0 + g * 32;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        st_global_v4(dst + 4 * i,
+                     make_uint4(__float_as_uint(v[4 * i]), __float_as_uint(v[4 * i + 1]),
+                                __float_as_uint(v[4 * i + 2]), __float_as_uint(v[4 * i + 3])));
+    } else {
+      void* out = p.out;
+      if (p.xchg) {
+        const TpDev* tp = p.guard.tp;
+        out = tp->part[tp->rank][tp->local->xcount & 1];
+      }
+      store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(out) + (long long)m * p.ldo + n0 + g * 32,
+                       v);
+    }
+  } else if constexpr (EPI == EPI_SWIGLU) {
+    if (!valid) return;
+    // tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows
+    sum.get(r, g * 16, BN / 2 + g * 16, v);
+    float o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i] = silu_f(v[i] * rs) * (v[16 + i] * rs);
+    store16_bf16(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)m * p.ldo + nb * (BN / 2) +
+                     g * 16,
+                 o);
+  } else {  // EPI_QKV
+    const int hh = g >> 2, q = g & 3;
+    const int col0 = n0 + hh * 128;  // the head's first column
+    const bool live = valid && col0 < p.q_cols + 2 * p.kv_cols;  // not the zero padding
+    const bool is_q = col0 < p.q_cols;
+    const bool is_v = col0 >= p.q_cols + p.kv_cols;
+    const float* bias = p.bias ? p.bias + col0 : nullptr;
+    const float* hn = is_v ? nullptr : (is_q ? p.q_norm : p.k_norm);
+    float ss = 0.f;
+    if (live) {
+      sum.get(r, hh * 128 + q * 16, hh * 128 + 64 + q * 16, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= rs;
+      if (bias) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          v[i] += __ldg(bias + q * 16 + i);
+          v[16 + i] += __ldg(bias + 64 + q * 16 + i);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) ss += v[i] * v[i];
+    }
+    if (hn != nullptr) {  // per-head RMSNorm (Qwen3): the head's 4 quarter sums, in order
+      float tot = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tot += __shfl_sync(0xffffffffu, ss, (lane & ~3) + j);
+      const float nscale = rsqrtf(tot * (1.f / 128.f) + p.norm_eps);
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          v[i] *= nscale * __ldg(hn + q * 16 + i);
+          v[16 + i] *= nscale * __ldg(hn + 64 + q * 16 + i);
+        }
+      }
+    }
+    if (!live) return;
+    const int pos = p.pos[m];
+    __nv_bfloat16* dst;
+    if (is_q) {
+      dst = p.qbuf + (long long)m * p.ldq + col0;
+    } else {
+      const int kv = is_v ? 1 : 0;
+      const int h = (col0 - p.q_cols - kv * p.kv_cols) >> 7;
+      const int page = p.tok_page[m];
+      dst = p.kv_layer +
+            ((((long long)page * 2 + kv) * p.n_kv_heads + h) * p.page_size + (pos % p.page_size)) *
+                128;
+    }
+    if (!is_v) {  // rotate-half RoPE: column j pairs with j + 64
+      const float4* cs = reinterpret_cast<const float4*>(p.rope + (long long)pos * 64) + q * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 t4 = __ldg(cs + i);  // (cos, sin) of pair columns 2i, 2i + 1
+        const float u1 = v[2 * i], u2 = v[16 + 2 * i];
+        const float w1 = v[2 * i + 1], w2 = v[16 + 2 * i + 1];
+        v[2 * i] = u1 * t4.x - u2 * t4.y;
+        v[16 + 2 * i] = u2 * t4.x + u1 * t4.y;
+        v[2 * i + 1] = w1 * t4.z - w2 * t4.w;
+        v[16 + 2 * i + 1] = w2 * t4.z + w1 * t4.w;
+      }
+    }
+    store16_bf16(dst + q * 16, v);
+    store16_bf16(dst + 64 + q * 16, v + 16);
+  }
+}
+
+// SPLIT: the instantiation that also runs tail split-K tiles (launched only when the launcher
+// chose splits > 1; the unsplit instantiation carries no split code and no extra registers).
+template <int BN, int EPI, int CG, bool SPLIT>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
@@ -136,6 +369,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int lane = lane_id();
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA rank inside the pair
   const bool leader = rank == 0;
+  if (threadIdx.x == 0) GEMM_STAMP(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -160,10 +394,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_STAMP(1);
   // Everything above overlaps the previous kernel's tail (programmatic dependent launch);
   // the boundary check and all data accesses come after the dependency resolves.
   grid_dep_wait();
   const bool run = guard_block(p.guard);
+  if (threadIdx.x == 0) GEMM_STAMP(2);
 
   const int num_m = (p.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
   const int unit0 = blockIdx.x / CG;      // this CTA (pair)'s first work unit
@@ -209,6 +445,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) {
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+            if (kb == kb0 && u == unit0) GEMM_STAMP(3);
             tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kGemmBK, row_a);
 #pragma unroll
             for (int h = 0; h < BN / 128; ++h)  // weight maps use 128-row boxes
@@ -245,6 +482,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (lane == 0 && kb == kb0 && u == unit0) GEMM_STAMP(4);
         if (lane == 0) {
           const uint64_t a0 = make_sdesc_sw128(smem_u32(sA + s * Cfg::A_BYTES), 16, 1024);
           const uint64_t b0 = make_sdesc_sw128(smem_u32(sB + s * Cfg::B_BYTES), 16, 1024);
@@ -268,11 +506,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) {
         if constexpr (CG == 1) tc_commit(&tfull[acc]);
         else tc_commit_2sm_mc(&tfull[acc], 0x3);
+        GEMM_STAMP(5);
       }
       __syncwarp();
     }
   } else if (warp >= 4) {
-    __shared__ int s_last;
     const int q = warp & 3;  // TMEM lane quadrant
     const int row = q * 32 + lane;
     int it = 0;
@@ -301,8 +539,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       float4* ws_tile =
           reinterpret_cast<float4*>(p.ws) + (long long)wtile * splits * (BN / 4) * kGemmBM;
       const uint32_t tacc = tbase + acc * BN + ((uint32_t)(q * 32) << 16);
-      if (splits > 1) {
+      if (SPLIT && splits > 1) {
         mbar_wait(&tfull[acc], acc_ph);
+        if (threadIdx.x == 128) GEMM_STAMP(6);
         tc_fence_after();
         // 1) this K-slice's partial tile -> workspace, TMEM released immediately
         float4* dst = ws_tile + (long long)split * (BN / 4) * kGemmBM + row;
@@ -311,26 +550,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t r[32];
           tmem_ld32(tacc + c * 32, r);
           tmem_ld_wait();
+          if (live) {  // dead rows (m >= M) are neither stored nor reduced
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            st_global_v4(dst + (c * 8 + i) * kGemmBM,
-                         make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]));
+            for (int i = 0; i < 8; ++i)
+              st_global_v4(dst + (c * 8 + i) * kGemmBM,
+                           make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]));
+          }
         }
+        if (threadIdx.x == 128) GEMM_STAMP(7);
         release_acc(acc);
-        // 2) ticket: the last K-slice of the tile reduces and runs the epilogue
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (row == 0) {
-          const int old = atomicAdd(&p.tickets[wtile], 1);
-          s_last = old == splits - 1;
-          if (s_last) p.tickets[wtile] = 0;
+        // 2) wait until all `splits` K-slices of this 128-row tile slot are stored. Safe to
+        //    spin: the launcher gives every CTA at most one split unit, as its last unit, and
+        //    the grid never exceeds one CTA (pair) per SM, so all siblings are resident.
+        int* tk = p.tickets + wtile;  // [0, 1024): arrivals, +1024: done
+        split_barrier(tk, splits);
+        if (threadIdx.x == 128) GEMM_STAMP(8);
+        // 3) this K-slice's share of the tile's (row, column-group) epilogue items, each the
+        //    split-order sum of the partials (deterministic) -- the reduction is spread over
+        //    all K-slice CTAs instead of one CTA reducing the whole tile
+        const int m_base = mb * Cfg::TILE_M + (int)rank * kGemmBM;
+        const int live_rows = min(kGemmBM, p.M - m_base);
+        const GmemSum gsum{ws_tile, splits};
+        // 8 items per row, row-major: a warp covers 4 whole rows
+        const int items = live_rows * 8;
+        for (int base = split * 128 + (row & ~31); base < items; base += splits * 128) {
+          const int item = base + lane;
+          const int r = item >> 3;
+          split_item_epilogue<EPI>(p, gsum, item < items, m_base + r, r, item & 7, n0, nb);
         }
+        if (threadIdx.x == 128) GEMM_STAMP(9);
+        // 4) the last K-slice through resets the tickets for the next launch
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (!s_last) continue;
-        __threadfence();
+        if (row == 0 && atomicAdd(tk + 1024, 1) == splits - 1) {
+          tk[0] = 0;
+          tk[1024] = 0;
+        }
+        continue;
       }
-      // Accumulator columns [col, col+32) of this thread's row: from TMEM, or the in-order sum
-      // of the split partials (split 0 first) -- the same bits whichever CTA arrives last.
+      // Unsplit tile: accumulator columns [col, col+32) of this thread's row from TMEM.
       // fused RMSNorm: the row's rsqrt factor (1 for epilogues without a norm in front)
       float rs = 1.f;
       if ((EPI == EPI_QKV || EPI == EPI_SWIGLU) && p.ssq_in != nullptr && live) {
@@ -340,43 +597,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         rs = rsqrtf(ssum / (float)(p.nseg * 256) + p.norm_eps_in);
       }
       auto load32 = [&](int col, float* v) {
-        if (splits == 1) {
-          uint32_t r[32];
-          tmem_ld32(tacc + col, r);
-          tmem_ld_wait();
+        uint32_t r[32];
+        tmem_ld32(tacc + col, r);
+        tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * rs;
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          for (int sp = 0; sp < splits; ++sp) {
-            const float4* src = ws_tile + ((long long)sp * (BN / 4) + col / 4) * kGemmBM + row;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 f = __ldcg(src + i * kGemmBM);
-              v[4 * i] += f.x;
-              v[4 * i + 1] += f.y;
-              v[4 * i + 2] += f.z;
-              v[4 * i + 3] += f.w;
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= rs;
-        }
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * rs;
       };
 
       if constexpr (EPI == EPI_RESID) {
         // residual row segment prefetched into registers while the MMA runs
         uint4 hres[BN / 8];
         __nv_bfloat16* hrow = p.resid + (long long)m * p.ldr + n0;
-        if (live && splits == 1) {
+        if (live) {
 #pragma unroll
           for (int i = 0; i < BN / 8; ++i) hres[i] = ld_global_v4(hrow + 8 * i);
         }
-        if (splits == 1) {
-          mbar_wait(&tfull[acc], acc_ph);
-          tc_fence_after();
-        }
+        mbar_wait(&tfull[acc], acc_ph);
+        if (threadIdx.x == 128) GEMM_STAMP(6);
+        tc_fence_after();
         float ss = 0.f;
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
@@ -385,7 +623,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (live) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const uint4 h = splits == 1 ? hres[c * 4 + i] : ld_global_v4(hrow + c * 32 + 8 * i);
+              const uint4 h = hres[c * 4 + i];
               const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -409,10 +647,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const TpDev* tp = p.guard.tp;
           out = tp->part[tp->rank][tp->local->xcount & 1];
         }
-        if (splits == 1) {
-          mbar_wait(&tfull[acc], acc_ph);
-          tc_fence_after();
-        }
+        mbar_wait(&tfull[acc], acc_ph);
+        if (threadIdx.x == 128) GEMM_STAMP(6);
+        tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           float v[32];
@@ -434,10 +671,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
-        if (splits == 1) {
-          mbar_wait(&tfull[acc], acc_ph);
-          tc_fence_after();
-        }
+        mbar_wait(&tfull[acc], acc_ph);
+        if (threadIdx.x == 128) GEMM_STAMP(6);
+        tc_fence_after();
         // Tile columns [0, BN/2) are gate rows, [BN/2, BN) the matching up rows.
 #pragma unroll 1
         for (int c = 0; c < BN / 64; ++c) {
@@ -464,10 +700,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) cs[i] = __ldg(src + i);
         }
-        if (splits == 1) {
-          mbar_wait(&tfull[acc], acc_ph);
-          tc_fence_after();
-        }
+        mbar_wait(&tfull[acc], acc_ph);
+        if (threadIdx.x == 128) GEMM_STAMP(6);
+        tc_fence_after();
 #pragma unroll
         for (int hh = 0; hh < BN / 128; ++hh) {
           const int col0 = n0 + hh * 128;
@@ -541,15 +776,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
-      if (splits == 1) release_acc(acc);
+      if (threadIdx.x == 128) GEMM_STAMP(7);
+      release_acc(acc);
     }
     if (EPI == EPI_STORE_BF16 && p.xchg) __threadfence_system();  // partials visible to peers
   }
 
+  if (threadIdx.x == 0) GEMM_STAMP(10);
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/arrivals are all done
   else __syncthreads();
   if (EPI == EPI_STORE_BF16 && p.xchg && run && threadIdx.x == 0) tp_publish_partial(p.guard.tp);
+  if (threadIdx.x == 64) GEMM_STAMP(11);
   if (warp == 2) {
     tc_fence_after();
     if constexpr (CG == 2) tmem_dealloc_2sm<Cfg::TMEM_COLS>(tbase);

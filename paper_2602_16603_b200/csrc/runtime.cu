@@ -206,6 +206,7 @@ struct fp_ctx {
   // split-K workspace (one prefill stream: launches are serialised, one buffer suffices)
   float* ws = nullptr;
   int* tickets = nullptr;
+  unsigned long long* gemm_dbg = nullptr;  // FP_GEMM_STAMPS=1: phase stamps of fp_op_gemm launches
   bool use_pair_gemm = true;
   int force_splits = 0;   // FP_FORCE_SPLITS (experiments)
   int force_pair = -1;    // FP_FORCE_PAIR (experiments): 0 single, 1 pair
@@ -273,29 +274,42 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // waves run unsplit; the remainder tiles (the partial last wave, or all tiles of a small
 // prefill chunk) are cut into S K-slices. Cost model in k-block units: waves * (k-blocks per
 // slice + fixed) + partial write/reduce traffic per split. Shape-only, so deterministic.
-static double choose_splits(int tiles, int num_k, int num_sms, int* full_tiles, int* splits) {
+// Split-K of the persistent kernel: the partial last wave (rem tiles; all tiles for short
+// requests) is cut into S K-slices, one unit per CTA (pair) of a single extra round, so the S
+// K-slice CTAs of a tile are co-resident and reduce it together (gemm.cuh split path). Cost in
+// k-block units (one 128 x 256 x 64 MMA step, ~0.34 us): a unit costs its K-slice plus ~4
+// k-blocks of pipeline fill; a split adds kSplitOverheadKb for the partial round trip through
+// L2, the inter-CTA barrier and the reduction (~8 us measured on B200, tools/split_sweep.py and
+// tools/gemm_stamps.py). A split must win by > 15%. tail_ok = false restricts splitting to
+// launches whose tiles all split (no full wave in front).
+static constexpr double kSplitOverheadKb = 24.0;
+static constexpr double kSplitOverheadKbQkv = 40.0;  // RoPE / KV-scatter items cost more
+// Tails behind full waves split only for long K (down_proj): the split-capable instantiation
+// runs the full-wave tiles with more register pressure (measured slower for QKV / SwiGLU).
+static bool split_tail_ok(int epi, int K) {
+  return epi != EPI_QKV && epi != EPI_SWIGLU && K / kGemmBK >= 128;
+}
+static double split_overhead(int epi) {
+  return epi == EPI_QKV ? kSplitOverheadKbQkv : kSplitOverheadKb;
+}
+static double choose_splits(int tiles, int num_k, int num_sms, int* full_tiles, int* splits,
+                            bool tail_ok = true, double overhead = kSplitOverheadKb) {
   const int rem = tiles % num_sms;
   const double full_cost = (double)(tiles / num_sms) * (num_k + 4.0);
-  *full_tiles = tiles - rem;
+  *full_tiles = tiles;
   *splits = 1;
-  // Measured on B200 (tools/split_sweep.py): a K-slice costs ~15 us of partial traffic and
-  // reduction regardless of its length, so splitting only pays for long-K GEMMs (down_proj,
-  // K = 14336) whose remainder is under half a wave.
-  if (rem == 0 || num_k < 128 || rem * 2 > num_sms) {
-    if (rem) *full_tiles = tiles;
-    return full_cost + (rem ? num_k + 4.0 : 0.0);
-  }
-  double best_t = 1e30;
-  for (int S = 1; S <= 8; ++S) {
-    if (S > 1 && (num_k / S < 4 || rem * S > 2 * num_sms)) break;
-    const double waves = std::ceil((double)rem * S / num_sms);
-    const double t = waves * ((double)num_k / S + 4.0) + (S > 1 ? 5.0 * S : 0.0);
-    if (t < best_t - 1e-9) {
-      best_t = t;
-      *splits = S;
+  const double unsplit = rem ? num_k + 4.0 : 0.0;
+  double best_t = unsplit;
+  if (rem && (tail_ok || tiles < num_sms)) {
+    for (int S = 2; S <= 32 && rem * S <= num_sms && num_k / S >= 4; ++S) {
+      const double t = std::ceil((double)num_k / S) + 4.0 + overhead;
+      if (t < best_t - 1e-9 && t < 0.85 * unsplit) {
+        best_t = t;
+        *splits = S;
+        *full_tiles = tiles - rem;
+      }
     }
   }
-  if (*splits == 1) *full_tiles = tiles;
   return full_cost + best_t;
 }
 
@@ -304,11 +318,12 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
                            cudaStream_t st) {
   constexpr int BN = 256;
   using Cfg = GemmCfg<BN, CG>;
-  auto kern = gemm_bf16_tn_kernel<BN, EPI, CG>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    for (auto k : {gemm_bf16_tn_kernel<BN, EPI, CG, false>, gemm_bf16_tn_kernel<BN, EPI, CG, true>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+      if (CG == 2) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    }
     attr = true;
   }
   const int tiles = ((p.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * (p.N / BN);
@@ -316,13 +331,21 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   p.splits = 1;
   p.full_tiles = tiles;
   if (c->ws && EPI != EPI_STORE_F32)
-    choose_splits(tiles, p.K / kGemmBK, slots, &p.full_tiles, &p.splits);
+    choose_splits(tiles, p.K / kGemmBK, slots, &p.full_tiles, &p.splits, split_tail_ok(EPI, p.K),
+                  split_overhead(EPI));
   if (c->force_splits > 0) {  // experiments only (FP_FORCE_SPLITS)
     const int rem = tiles % slots;
-    p.splits = c->force_splits;
-    p.full_tiles = (p.splits > 1 && rem) ? tiles - rem : tiles;
-    if (p.splits > 1 && rem == 0) p.full_tiles = tiles;
+    p.splits = rem ? c->force_splits : 1;
+    p.full_tiles = tiles - rem;
   }
+  // K-slices must be non-empty; the split units must fit one round (one per CTA: the K-slice
+  // CTAs of a tile wait for each other) and the workspace / ticket slots
+  const int num_k = p.K / kGemmBK;
+  while (p.splits > 1 && ((p.splits - 1) * ((num_k + p.splits - 1) / p.splits) >= num_k ||
+                          (tiles - p.full_tiles) * p.splits > slots ||
+                          (long long)(tiles - p.full_tiles) * CG * p.splits > 8LL * c->num_sms))
+    --p.splits;
+  if (p.splits == 1) p.full_tiles = tiles;
   p.ws = c->ws;
   p.tickets = c->tickets;
   const int units = p.full_tiles + (tiles - p.full_tiles) * p.splits;
@@ -341,27 +364,31 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, kern, a, b, p);
+  if (p.splits > 1) cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, true>, a, b, p);
+  else cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, false>, a, b, p);
 }
 
 // Pair (2-CTA, 256-row) tiles or single-CTA (128-row) tiles, whichever the cost model
 // predicts faster for this shape: pair tiles run the mainloop ~9% faster per SM (measured on
 // B200: less shared-memory traffic per k-block) but pad M to 256 rows and halve the number
 // of concurrent tiles. Shape-only decision.
-static bool pick_pair(const fp_ctx* c, int M, int N, int K) {
+static bool pick_pair(const fp_ctx* c, int epi, int M, int N, int K) {
   if (c->force_pair >= 0) return c->force_pair == 1 && M > kGemmBM;
   if (!c->use_pair_gemm || M <= kGemmBM) return false;
   int ft, sp;
   const int nN = N / 256, num_k = K / kGemmBK;
-  const double t1 = choose_splits(((M + 127) / 128) * nN, num_k, c->num_sms, &ft, &sp);
-  const double t2 = choose_splits(((M + 255) / 256) * nN, num_k, c->num_sms / 2, &ft, &sp) / 1.09;
+  const bool tail = split_tail_ok(epi, K);
+  const double ov = split_overhead(epi);
+  const double t1 = choose_splits(((M + 127) / 128) * nN, num_k, c->num_sms, &ft, &sp, tail, ov);
+  const double t2 =
+      choose_splits(((M + 255) / 256) * nN, num_k, c->num_sms / 2, &ft, &sp, tail, ov) / 1.09;
   return t2 < t1;
 }
 
 template <int EPI>
 static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
                         const GemmParams& p, cudaStream_t st) {
-  if (pick_pair(c, p.M, p.N, p.K)) launch_gemm_cg<EPI, 2>(c, a, b, p, st);
+  if (pick_pair(c, EPI, p.M, p.N, p.K)) launch_gemm_cg<EPI, 2>(c, a, b, p, st);
   else launch_gemm_cg<EPI, 1>(c, a, b, p, st);
 }
 
@@ -719,6 +746,8 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     if (const char* e = getenv("FP_PAIR_GEMM")) c->use_pair_gemm = atoi(e) != 0;
     if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
+    if (const char* e = getenv("FP_GEMM_STAMPS"))
+      if (atoi(e)) CK(cudaMalloc(&c->gemm_dbg, (size_t)4096 * 16 * sizeof(unsigned long long)));
     const uint64_t rows = (uint64_t)L * kv_pages * 2 * c->hkv * page_size;
     REQ(rows < (1ull << 31), "KV pool too large for 32-bit TMA row coordinates");
     int rc = make_map(&c->tm_kv, c->kv, rows, 128, 128);
@@ -767,6 +796,7 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaFree(c->kv);
   cudaFree(c->ws);
   cudaFree(c->tickets);
+  cudaFree(c->gemm_dbg);
   cudaFreeHost((void*)c->hctl);
   for (void* ptr : c->tp_opened) cudaIpcCloseMemHandle(ptr);
   cudaFree(c->tp_block);
@@ -794,6 +824,20 @@ int fp_ctx_free_pages(fp_ctx* c, int64_t* n) {
 int fp_ctx_set_window(fp_ctx* c, int32_t w) {
   REQ(c && w >= 1, "window must be >= 1");
   c->window = w;
+  return FP_OK;
+}
+int fp_debug_gemm_stamps(fp_ctx* c, uint64_t* out, int32_t max_ctas) {
+  REQ(c && out && max_ctas > 0, "bad arguments");
+  REQ(c->gemm_dbg != nullptr, "phase stamps disabled (set FP_GEMM_STAMPS=1 before fp_ctx_create)");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(out, c->gemm_dbg, (size_t)std::min(max_ctas, 4096) * 16 * sizeof(uint64_t),
+                cudaMemcpyDeviceToHost));
+  return FP_OK;
+}
+int fp_ctx_set_gemm_policy(fp_ctx* c, int32_t pair, int32_t splits) {
+  REQ(c && pair >= -1 && pair <= 1 && splits >= 0 && splits <= 32, "bad gemm policy");
+  c->force_pair = pair;
+  c->force_splits = splits;
   return FP_OK;
 }
 int fp_sync(fp_ctx* c) {
@@ -1422,6 +1466,10 @@ int fp_op_gemm(fp_ctx* c, int32_t epi, const void* A, const void* B, void* C, in
   p.resid = static_cast<__nv_bfloat16*>(C);
   p.ldr = N;
   std::lock_guard<std::mutex> lk(c->launch_mu);
+  if (c->gemm_dbg) {
+    CK(cudaMemsetAsync(c->gemm_dbg, 0, (size_t)4096 * 16 * sizeof(unsigned long long), c->stream));
+    p.dbg = c->gemm_dbg;
+  }
   if (epi == 0) launch_gemm<EPI_STORE_BF16>(c, ta, tb, p, c->stream);
   else if (epi == 1) launch_gemm<EPI_STORE_F32>(c, ta, tb, p, c->stream);
   else if (epi == 2) launch_gemm<EPI_RESID>(c, ta, tb, p, c->stream);

@@ -60,3 +60,42 @@ def test_rmsnorm(ctx, d):
     xf = x.float()
     ref = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5) * gm.float()
     assert (o.float() - ref).abs().max().item() <= 2 ** -7 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("M,N,K", [(42, 4096, 4096), (300, 1024, 4096), (77, 512, 14336),
+                                   (1, 256, 1024), (2000, 4096, 4096)])
+@pytest.mark.parametrize("pair,splits", [(0, 3), (0, 16), (1, 5), (1, 12)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_forced_split(ctx, M, N, K, pair, splits, epi):
+    """Forced split-K tiling (fp_ctx_set_gemm_policy): the K-slice CTAs of a tile reduce it
+    together; within bf16 tolerance of fp32 and bit-identical run to run (partials are summed
+    in split order)."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + splits + epi)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    if epi == 1:
+        R = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    else:
+        R = torch.randn(M, N, device="cuda", dtype=torch.bfloat16, generator=g)
+    ref = A.float() @ B.float().t() + (R.float() if epi == 2 else 0.0)
+    outs = []
+    try:
+        _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, pair, splits))
+        for _ in range(2):
+            out = R.clone()
+            torch.cuda.synchronize()
+            _lib.check(ctx.lib.fp_op_gemm(ctx.h, epi, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                          M, N, K))
+            ctx.sync()
+            outs.append(out)
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+    assert torch.equal(outs[0], outs[1])
+    err = (outs[0].float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    tol = 1e-5 * scale * K ** 0.5 if epi == 1 else 2 ** -7 * scale + 1e-3
+    assert err <= tol, (err, scale)

@@ -1,4 +1,10 @@
-"""Sweep forced split-K / pair settings for small-M shapes (run under different env vars)."""
+"""Sweep GEMM tiling (CTA pair vs single, forced split-K count) per shape with the weights
+streamed from HBM as inside a prefill step (rotating weight copies larger than L2).
+
+    python tools/split_sweep.py [--out gpurun_out/split_sweep.json]
+"""
+import argparse
+import json
 import os
 import sys
 
@@ -7,23 +13,60 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_16603_b200.config import SHAPES  # noqa: E402
 from paper_2602_16603_b200.native import PrefillContext  # noqa: E402
-from tools.gemm_bench import timeit  # noqa: E402
+
+SHAPES_NK = [(4096, 4096), (6144, 4096), (28672, 4096), (4096, 14336)]
+MS = [42, 163, 386, 545, 872, 1021, 1572, 2048, 3000]
+SPLITS = [1, 2, 3, 4, 6, 8, 12, 16]
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/split_sweep.json")
+    ap.add_argument("--iters", type=int, default=12)
+    a = ap.parse_args()
     ctx = PrefillContext(SHAPES["tiny"], kv_pages=8, max_pos=1024)
     st = torch.cuda.ExternalStream(ctx.stream_ptr)
-    tag = f"pair={os.environ.get('FP_FORCE_PAIR', 'auto')} S={os.environ.get('FP_FORCE_SPLITS', 'auto')}"
-    out = []
-    for N, K in [(4096, 4096), (4096, 14336), (28672, 4096), (6144, 4096)]:
-        B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16)
-        for M in [163, 545, 1024, 1572]:
+    lib = ctx.lib
+    res = []
+    for N, K in SHAPES_NK:
+        copies = max(2, int(400e6 // (N * K * 2)) + 1)  # > 3x L2 of weights in rotation
+        Bs = [torch.randn(N, K, device="cuda", dtype=torch.bfloat16) for _ in range(copies)]
+        for M in MS:
             A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
-            C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-            t = timeit(lambda: ctx.lib.fp_op_gemm(ctx.h, 2, A.data_ptr(), B.data_ptr(), C.data_ptr(),
-                                                  M, N, K), st)
-            out.append(f"{N}x{K} M={M}:{t:7.1f}")
-    print(tag, " | ".join(out), flush=True)
+            C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+            for pair, S in [(-1, 0)] + [(pair, S) for pair in (0, 1) for S in SPLITS]:
+                if True:
+                    lib.fp_ctx_set_gemm_policy(ctx.h, pair, S)
+                    i = [0]
+
+                    def call():
+                        B = Bs[i[0] % copies]
+                        i[0] += 1
+                        lib.fp_op_gemm(ctx.h, 2, A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K)
+
+                    for _ in range(3):
+                        call()
+                    torch.cuda.synchronize()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    for _ in range(a.iters):
+                        call()
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    us = e0.elapsed_time(e1) / a.iters * 1e3
+                    res.append({"N": N, "K": K, "M": M, "pair": pair, "S": S,
+                                "us": round(us, 2)})
+            lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+            best = min((r for r in res if r["N"] == N and r["K"] == K and r["M"] == M),
+                       key=lambda r: r["us"])
+            print(f"N={N} K={K} M={M}: best pair={best['pair']} S={best['S']} "
+                  f"{best['us']} us",
+                  flush=True)
+        del Bs
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as fh:
+        json.dump(res, fh)
     ctx.close()
 
 
