@@ -7,17 +7,25 @@
 // cache, one 128-token page per KV tile, so tiles sit at ABSOLUTE request positions and a query
 // row's result is independent of chunking and batch composition.
 //
-// CTA = one 128-row query tile x two query heads of the same KV head (GQA pair), so both heads
-// share every K/V tile in shared memory. Warp roles (320 threads, 1 CTA/SM):
-//   warp 0       TMA producer: Q tiles once, then K_j, V_j into a 3-slot ring (pages via the
-//                block table; 128B-swizzled 64-column boxes)
+// Work item = one 128-row query tile x two query heads of the same KV head (GQA pair): both
+// heads share every K/V tile in shared memory. The kernel is PERSISTENT: one CTA per SM takes
+// work items from a global counter in longest-first order (the host sorts query tiles by KV
+// length), so the causal imbalance between tiles is absorbed dynamically, and the next item's Q
+// load and first S = QK^T overlap the current item's last P*V and output epilogue.
+// Warp roles (320 threads, 1 CTA/SM):
+//   warp 0       scheduler + TMA producer: fetches work, Q tiles, then K_j, V_j into a 3-slot
+//                ring (pages via the block table; 128B-swizzled 64-column boxes)
 //   warp 1       TMEM allocator + single-thread MMA issuer:
 //                  S_h = Q_h K_j^T      (SS, M=128 N=128 K=128, fp32 accumulators in TMEM)
 //                  O_h += P_h V_j       (TS: P read from TMEM, V MN-major from smem)
 //                issued ping-pong so head 1's MMAs overlap head 0's softmax and vice versa
 //   warps 2-5    softmax for head 0, warps 6-9 softmax for head 1: one query row per thread,
-//                exp2 online softmax, lazy O rescale (only when the row max grows by > 2^8),
+//                exp2 online softmax with lazy O rescale (only when the row max grows by > 2^8),
 //                P written back to TMEM over S as bf16, final O / l epilogue to HBM.
+// Softmax arithmetic is budgeted against the tensor pipe: the scale is folded into one packed
+// FFMA2 per element pair, row sums use packed FADD2, and 3 of every 8 exponentials run as a
+// degree-3 polynomial on the FMA pipe (Cody-Waite split, |rel err| < 1.1e-4 -- below the bf16
+// rounding P gets anyway) so the 16/clk/SM MUFU.EX2 rate does not bound the loop.
 // TMEM columns: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
 #pragma once
 #include "common.cuh"
@@ -33,7 +41,7 @@ struct AttnTile {
 };
 
 struct AttnTcParams {
-  const AttnTile* items;
+  const AttnTile* items;          // query tiles, longest KV range first
   int n_items;
   int n_heads, n_kv_heads;
   int pairs_per_kv;               // ceil((n_heads / n_kv_heads) / 2)
@@ -44,6 +52,7 @@ struct AttnTcParams {
   long long kv_row_layer;         // row of (layer, page 0, k, head 0, slot 0) in the pool map
   int kv_rows_per_page;           // 2 * n_kv_heads * 128 rows per page (one layer)
   float scale_log2;               // log2(e) / sqrt(128)
+  int* sched;                     // [2] work counter, finished CTAs (zero between launches)
   Guard guard;
 };
 
@@ -53,9 +62,81 @@ constexpr int TILE = 128;
 constexpr int TILE_BYTES = 128 * 128 * 2;  // 32 KB: two 64-column swizzle atoms of 16 KB
 constexpr int ATOM_BYTES = 16384;
 constexpr int STAGES = 3;
-constexpr int SMEM_BYTES = 1024 + 2 * TILE_BYTES + STAGES * TILE_BYTES + 256;
+constexpr int SMEM_BYTES = 1024 + 2 * TILE_BYTES + STAGES * TILE_BYTES + 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: rescale O only if max grows > 256x
+constexpr int SOFTMAX_WARPS = 8;
 }  // namespace tcattn
+
+// ---- packed fp32 pairs (sm_100 FFMA2 / FADD2) -----------------------------------------------
+DEVI float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+DEVI float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+// 2^x for x <= 0 (or -inf) on the FMA pipe: x = j + f, j = rint(x), f in [-1/2, 1/2];
+// 2^f ~ 1 + f (c1 + f (c2 + f c3)); 2^j by adding j to the exponent field.
+DEVI float2 exp2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: x + magic rounds x to an integer
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 j = fadd2(t, make_float2(-kMagic, -kMagic));
+  const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+  float2 p = ffma2(f, make_float2(0.05500892549753189f, 0.05500892549753189f),
+                   make_float2(0.2422109991312027f, 0.2422109991312027f));
+  p = ffma2(p, f, make_float2(0.693282961845398f, 0.693282961845398f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  // low bits of t hold j (two's complement): add j << 23 to the exponent
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+DEVI void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+// decoded work item
+struct AttnWork {
+  AttnTile it;
+  int head0, head1;
+  bool has_head1;
+  int kvh;
+  int n_tiles;
+};
+
+DEVI AttnWork attn_decode(const AttnTcParams& p, int w) {
+  const int hp = p.n_kv_heads * p.pairs_per_kv;
+  AttnWork a;
+  a.it = p.items[w / hp];
+  const int y = w % hp;
+  a.kvh = y / p.pairs_per_kv;
+  const int pair = y % p.pairs_per_kv;
+  const int group = p.n_heads / p.n_kv_heads;
+  a.head0 = a.kvh * group + 2 * pair;
+  a.has_head1 = 2 * pair + 1 < group;
+  a.head1 = a.has_head1 ? a.head0 + 1 : a.head0;
+  a.n_tiles = (a.it.q_pos0 + a.it.n_rows + tcattn::TILE - 1) / tcattn::TILE;
+  return a;
+}
 
 __global__ void __launch_bounds__(tcattn::THREADS, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -68,13 +149,17 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   uint8_t* sKV = smem + 2 * TILE_BYTES;    // [STAGES][TILE_BYTES]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + STAGES * TILE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;
   uint64_t* kv_empty = kv_full + STAGES;
   uint64_t* s_full = kv_empty + STAGES;  // [2]
   uint64_t* p_full = s_full + 2;         // [2]
   uint64_t* o_full = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
-
+  uint64_t* o_empty = o_full + 1;        // [2]
+  uint64_t* w_full = o_empty + 2;        // [2] work ring
+  uint64_t* w_empty = w_full + 2;        // [2]
+  int* w_ring = reinterpret_cast<int*>(w_empty + 2);  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_ring + 2);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -83,6 +168,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmKV);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -90,6 +176,9 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     for (int h = 0; h < 2; ++h) {
       mbar_init(&s_full[h], 1);
       mbar_init(&p_full[h], 128);
+      mbar_init(&o_empty[h], 128);
+      mbar_init(&w_full[h], 1);
+      mbar_init(&w_empty[h], 1 + SOFTMAX_WARPS);
     }
     mbar_init(o_full, 1);
     fence_barrier_init();
@@ -101,47 +190,57 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   const uint32_t tbase = *tmem_slot;
   grid_dep_wait();
   const bool run = guard_block(p.guard);
-
-  const AttnTile it = p.items[blockIdx.x];
-  const int kvh = blockIdx.y / p.pairs_per_kv;
-  const int pair = blockIdx.y % p.pairs_per_kv;
-  const int group = p.n_heads / p.n_kv_heads;
-  const int head0 = kvh * group + 2 * pair;
-  const bool has_head1 = 2 * pair + 1 < group;
-  const int head1 = has_head1 ? head0 + 1 : head0;
-  const int kv_len = it.q_pos0 + it.n_rows;
-  const int n_tiles = (kv_len + TILE - 1) / TILE;
-  const int* bt = p.block_table + (long long)it.req * p.bt_stride;
+  const int n_work = p.n_items * p.n_kv_heads * p.pairs_per_kv;
 
   if (!run) {
     // stopped at this boundary: nothing to do
   } else if (warp == 0) {
-    // ------------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ scheduler + TMA producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_last();  // K/V tiles are re-read by other q tiles
-      mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
-      for (int h = 0; h < 2; ++h) {
-        const int col = (h ? head1 : head0) * 128;
-        tma_load_2d(sQ + h * TILE_BYTES, &tmQ, q_full, col, it.q_row0);
-        tma_load_2d(sQ + h * TILE_BYTES + ATOM_BYTES, &tmQ, q_full, col + 64, it.q_row0);
-      }
-      int s = 0;
-      uint32_t ph = 0;
-      for (int j = 0; j < n_tiles; ++j) {
-        const long long page = bt[j];  // page_size == TILE
-        for (int kv = 0; kv < 2; ++kv) {
-          mbar_wait(&kv_empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&kv_full[s], TILE_BYTES);
-          const long long row =
-              p.kv_row_layer + page * p.kv_rows_per_page + (long long)(kv * p.n_kv_heads + kvh) * TILE;
-          tma_load_2d_hint(sKV + s * TILE_BYTES, &tmKV, &kv_full[s], 0, (int)row, pol);
-          tma_load_2d_hint(sKV + s * TILE_BYTES + ATOM_BYTES, &tmKV, &kv_full[s], 64, (int)row,
-                           pol);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+      int s = 0, ws = 0, it = 0;
+      uint32_t ph = 0, wph = 0;
+      for (;;) {
+        // first item static (CTA b takes item b); later ones from the global counter, which
+        // launches with no more items than CTAs never touch
+        int w = it == 0 ? (int)blockIdx.x
+                        : (n_work > (int)gridDim.x ? (int)gridDim.x + atomicAdd(&p.sched[0], 1)
+                                                   : n_work);
+        if (w >= n_work) w = -1;
+        mbar_wait(&w_empty[ws], wph ^ 1);
+        w_ring[ws] = w;
+        mbar_arrive(&w_full[ws]);
+        if (++ws == 2) {
+          ws = 0;
+          wph ^= 1;
+        }
+        if (w < 0) break;
+        const AttnWork a = attn_decode(p, w);
+        const int* bt = p.block_table + (long long)a.it.req * p.bt_stride;
+        mbar_wait(q_empty, (it & 1) ^ 1);  // the previous item's last QK^T has run
+        mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
+        for (int h = 0; h < 2; ++h) {
+          const int col = (h ? a.head1 : a.head0) * 128;
+          tma_load_2d(sQ + h * TILE_BYTES, &tmQ, q_full, col, a.it.q_row0);
+          tma_load_2d(sQ + h * TILE_BYTES + ATOM_BYTES, &tmQ, q_full, col + 64, a.it.q_row0);
+        }
+        for (int j = 0; j < a.n_tiles; ++j) {
+          const long long page = bt[j];  // page_size == TILE
+          for (int kv = 0; kv < 2; ++kv) {
+            mbar_wait(&kv_empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&kv_full[s], TILE_BYTES);
+            const long long row = p.kv_row_layer + page * p.kv_rows_per_page +
+                                  (long long)(kv * p.n_kv_heads + a.kvh) * TILE;
+            tma_load_2d_hint(sKV + s * TILE_BYTES, &tmKV, &kv_full[s], 0, (int)row, pol);
+            tma_load_2d_hint(sKV + s * TILE_BYTES + ATOM_BYTES, &tmKV, &kv_full[s], 64, (int)row,
+                             pol);
+            if (++s == STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
+        ++it;
       }
     }
     __syncwarp();
@@ -151,7 +250,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     constexpr uint32_t idesc_pv = make_idesc_bf16(128, 128, true);  // V is MN-major
     const uint32_t tS[2] = {tbase, tbase + 128};
     const uint32_t tO[2] = {tbase + 256, tbase + 384};
-    uint32_t seq = 0;  // ring sequence number of the next tile to consume
+    uint32_t seq = 0;  // ring sequence number of the next K/V tile to consume
     auto slot_of = [&](uint32_t sq) { return (int)(sq % STAGES); };
     auto wait_tile = [&](uint32_t sq) { mbar_wait(&kv_full[slot_of(sq)], (sq / STAGES) & 1); };
     auto issue_qk = [&](int h, uint32_t ksq) {
@@ -172,52 +271,73 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
                      idesc_pv, (acc || kk > 0) ? 1u : 0u);
       }
     };
-    mbar_wait(q_full, 0);
-    wait_tile(0);
-    tc_fence_after();
-    if (lane == 0) {
-      issue_qk(0, 0);
-      tc_commit(&s_full[0]);
-      issue_qk(1, 0);
-      tc_commit(&s_full[1]);
-      tc_commit(&kv_empty[slot_of(0)]);
-    }
-    __syncwarp();
-    seq = 1;
-    for (int j = 0; j < n_tiles; ++j) {
-      const bool last = j == n_tiles - 1;
-      const uint32_t vsq = seq;      // V_j
-      const uint32_t ksq = seq + 1;  // K_{j+1}
-      wait_tile(vsq);
-      mbar_wait(&p_full[0], j & 1);
-      tc_fence_after();
-      if (lane == 0) issue_pv(0, vsq, j > 0);
+    int ws = 0, it = 0;
+    uint32_t wph = 0, tc = 0;  // tc: tiles consumed before this item (s_full / p_full phases)
+    for (;;) {
+      mbar_wait(&w_full[ws], wph);
+      const int w = w_ring[ws];
       __syncwarp();
-      if (!last) {
-        wait_tile(ksq);
-        tc_fence_after();
-        if (lane == 0) {
-          issue_qk(0, ksq);
-          tc_commit(&s_full[0]);
-        }
-        __syncwarp();
+      if (lane == 0) mbar_arrive(&w_empty[ws]);
+      if (++ws == 2) {
+        ws = 0;
+        wph ^= 1;
       }
-      mbar_wait(&p_full[1], j & 1);
+      if (w < 0) break;
+      const int n_tiles = attn_decode(p, w).n_tiles;
+      mbar_wait(q_full, it & 1);
+      wait_tile(seq);
       tc_fence_after();
       if (lane == 0) {
-        issue_pv(1, vsq, j > 0);
-        tc_commit(&kv_empty[slot_of(vsq)]);
-        if (!last) {
-          issue_qk(1, ksq);
-          tc_commit(&s_full[1]);
-          tc_commit(&kv_empty[slot_of(ksq)]);
-        }
+        issue_qk(0, seq);
+        tc_commit(&s_full[0]);
+        issue_qk(1, seq);
+        tc_commit(&s_full[1]);
+        tc_commit(&kv_empty[slot_of(seq)]);
+        if (n_tiles == 1) tc_commit(q_empty);
       }
       __syncwarp();
-      seq += 2;
+      ++seq;
+      for (int j = 0; j < n_tiles; ++j) {
+        const bool last = j == n_tiles - 1;
+        const uint32_t vsq = seq;      // V_j
+        const uint32_t ksq = seq + 1;  // K_{j+1}
+        const uint32_t tph = (tc + j) & 1;
+        wait_tile(vsq);
+        mbar_wait(&p_full[0], tph);
+        if (j == 0) mbar_wait(&o_empty[0], (it & 1) ^ 1);  // previous item's O0 drained
+        tc_fence_after();
+        if (lane == 0) issue_pv(0, vsq, j > 0);
+        __syncwarp();
+        if (!last) {
+          wait_tile(ksq);
+          tc_fence_after();
+          if (lane == 0) {
+            issue_qk(0, ksq);
+            tc_commit(&s_full[0]);
+          }
+          __syncwarp();
+        }
+        mbar_wait(&p_full[1], tph);
+        if (j == 0) mbar_wait(&o_empty[1], (it & 1) ^ 1);
+        tc_fence_after();
+        if (lane == 0) {
+          issue_pv(1, vsq, j > 0);
+          tc_commit(&kv_empty[slot_of(vsq)]);
+          if (!last) {
+            issue_qk(1, ksq);
+            tc_commit(&s_full[1]);
+            tc_commit(&kv_empty[slot_of(ksq)]);
+            if (j + 1 == n_tiles - 1) tc_commit(q_empty);  // last QK^T of the item issued
+          }
+        }
+        __syncwarp();
+        seq += last ? 1 : 2;  // the last step consumes V only; the next item's K_0 follows
+      }
+      if (lane == 0) tc_commit(o_full);
+      __syncwarp();
+      tc += n_tiles;
+      ++it;
     }
-    if (lane == 0) tc_commit(o_full);
-    __syncwarp();
   } else {
     // ------------------------------------------------------------------ softmax + epilogue
     const int h = (warp - 2) >> 2;  // 0: warps 2-5, 1: warps 6-9
@@ -226,100 +346,134 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t tS = tbase + h * 128 + lane_off;
     const uint32_t tO = tbase + 256 + h * 128 + lane_off;
-    const int qpos = it.q_pos0 + row;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(&s_full[h], j & 1);
+    const float sc = p.scale_log2;
+    int ws = 0, it = 0;
+    uint32_t wph = 0, tc = 0;
+    for (;;) {
+      mbar_wait(&w_full[ws], wph);
+      const int w = w_ring[ws];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&w_empty[ws]);
+      if (++ws == 2) {
+        ws = 0;
+        wph ^= 1;
+      }
+      if (w < 0) break;
+      const AttnWork a = attn_decode(p, w);
+      const int qpos = a.it.q_pos0 + row;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < a.n_tiles; ++j) {
+        mbar_wait(&s_full[h], (tc + j) & 1);
+        tc_fence_after();
+        uint32_t su[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, su[c]);
+        tmem_ld_wait();
+        float sr[128];
+#pragma unroll
+        for (int i = 0; i < 128; ++i) sr[i] = __uint_as_float(su[i >> 5][i & 31]);
+        const int kv0 = j * TILE;
+        if (kv0 + TILE - 1 > a.it.q_pos0) {  // diagonal tile: causal mask
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (kv0 + i > qpos) sr[i] = -INFINITY;
+        }
+        float mx = sr[0];
+#pragma unroll
+        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, sr[i]);
+        const float m_new = fmaxf(m, mx * sc);  // scaled (log2) units
+        if (j == 0) {
+          m = m_new;
+        } else {
+          const bool need = m_new > m + RESCALE_THRESHOLD;
+          if (__any_sync(0xffffffffu, need)) {
+            const float alpha = need ? fast_exp2(m - m_new) : 1.f;
+            if (need) {
+              l *= alpha;
+              m = m_new;
+            }
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld32(tO + c * 32, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(tO + c * 32, o);
+            }
+            tmem_st_wait();
+          }
+        }
+        const float nm = (m == -INFINITY) ? 0.f : -m;
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float2 x = ffma2(make_float2(sr[c * 32 + i], sr[c * 32 + i + 1]),
+                                   make_float2(sc, sc), make_float2(nm, nm));
+            float2 e;
+            if ((i & 15) < 6) {  // 3 of every 8 exponentials on the FMA pipe
+              e = exp2_poly2(x);
+            } else {
+              e.x = fast_exp2(x.x);
+              e.y = fast_exp2(x.y);
+            }
+            if (i & 2) acc1 = fadd2(acc1, e);
+            else acc0 = fadd2(acc0, e);
+            pk[i >> 1] = pack_bf16x2(e.x, e.y);
+          }
+          tmem_st16(tS + c * 16, pk);  // P (bf16 pairs) over the consumed S columns
+        }
+        l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[h]);
+      }
+      // epilogue: O / l -> bf16 -> HBM, then release O for the next item's first P*V
+      mbar_wait(o_full, it & 1);
       tc_fence_after();
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, sr[c]);
-      tmem_ld_wait();
-      const int kv0 = j * TILE;
-      const bool diag = kv0 + TILE - 1 > it.q_pos0;
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float v = __uint_as_float(sr[c][i]) * p.scale_log2;
-          if (diag && kv0 + c * 32 + i > qpos) v = -INFINITY;
-          sr[c][i] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
-        }
-      }
-      const float m_new = fmaxf(m, mx);
-      if (j == 0) {
-        m = m_new;
-      } else {
-        const bool need = m_new > m + RESCALE_THRESHOLD;
-        if (__any_sync(0xffffffffu, need)) {
-          const float alpha = need ? fast_exp2(m - m_new) : 1.f;
-          if (need) {
-            l *= alpha;
-            m = m_new;
-          }
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const bool live = row < a.it.n_rows && (h == 0 || a.has_head1);
+      __nv_bfloat16* dst =
+          p.out + (long long)(a.it.q_row0 + row) * p.ldo + (h ? a.head1 : a.head0) * 128;
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(tO + c * 32, o);
-          }
-          tmem_st_wait();
-        }
-      }
-      const float msub = (m == -INFINITY) ? 0.f : m;
-      float sum = 0.f;
-      uint32_t pk[2][32];
-#pragma unroll
       for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_ld_wait();
+        if (live) {
+          float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = fast_exp2(__uint_as_float(sr[c][i]) - msub);
-          const float p1 = fast_exp2(__uint_as_float(sr[c][i + 1]) - msub);
-          sum += p0 + p1;
-          pk[c >> 1][(c & 1) * 16 + (i >> 1)] = pack_bf16x2(p0, p1);
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * inv;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 u;
+            u.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+            u.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+            u.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+            u.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+            st_global_v4(dst + c * 32 + 8 * i, u);
+          }
         }
       }
-      l += sum;
-      tmem_st32(tS, pk[0]);
-      tmem_st32(tS + 32, pk[1]);
-      tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&p_full[h]);
-    }
-    // epilogue: O / l -> bf16 -> HBM
-    mbar_wait(o_full, 0);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const bool live = row < it.n_rows && (h == 0 || has_head1);
-    __nv_bfloat16* dst = p.out + (long long)(it.q_row0 + row) * p.ldo + (h ? head1 : head0) * 128;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tmem_ld32(tO + c * 32, o);
-      tmem_ld_wait();
-      if (live) {
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * inv;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint4 u;
-          u.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
-          u.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
-          u.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
-          u.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
-          st_global_v4(dst + c * 32 + 8 * i, u);
-        }
-      }
+      mbar_arrive(&o_empty[h]);
+      tc += a.n_tiles;
+      ++it;
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (run && n_work > (int)gridDim.x && threadIdx.x == 0) {  // last CTA out re-arms the counter
+    __threadfence();
+    if (atomicAdd(&p.sched[1], 1) == (int)gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);

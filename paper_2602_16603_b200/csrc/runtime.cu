@@ -206,6 +206,7 @@ struct fp_ctx {
   // split-K workspace (one prefill stream: launches are serialised, one buffer suffices)
   float* ws = nullptr;
   int* tickets = nullptr;
+  int* attn_sched = nullptr;  // persistent attention work counter (self-resetting)
   unsigned long long* gemm_dbg = nullptr;  // FP_GEMM_STAMPS=1: phase stamps of fp_op_gemm launches
   bool use_pair_gemm = true;
   int force_splits = 0;   // FP_FORCE_SPLITS (experiments)
@@ -400,17 +401,18 @@ static int launch_rms(const RmsParams& p, cudaStream_t st) {
   return FP_OK;
 }
 
-static void launch_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const AttnTcParams& p,
-                        cudaStream_t st) {
+static void launch_attn(const fp_ctx* c, const CUtensorMap& tq, const CUtensorMap& tkv,
+                        const AttnTcParams& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          tcattn::SMEM_BYTES);
     attr = true;
   }
-  dim3 grid(p.n_items, p.n_kv_heads * p.pairs_per_kv);
-  launch_pdl(attn_prefill_tc_kernel, grid, dim3(tcattn::THREADS), tcattn::SMEM_BYTES, st, tq, tkv,
-             p);
+  // persistent: one CTA per SM (at most one per work item), work taken longest-first
+  const int n_work = p.n_items * p.n_kv_heads * p.pairs_per_kv;
+  launch_pdl(attn_prefill_tc_kernel, dim3(std::min(n_work, c->num_sms)), dim3(tcattn::THREADS),
+             tcattn::SMEM_BYTES, st, tq, tkv, p);
 }
 
 static bool boundary_eligible(const fp_ctx* c, int gran, int i, int n_entries) {
@@ -529,10 +531,11 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
     a.kv_row_layer = (long long)layer * c->kv_pages * 2 * c->hkv * c->page_size;
     a.kv_rows_per_page = 2 * c->hkv * c->page_size;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)m.head_dim);
+    a.sched = c->attn_sched;
     a.guard = g;
     if (a.n_items > 0) {
       ProfScope ps(c, st, FP_K_ATTN, layer, M, ch.attn_flops, 0.0);
-      launch_attn(t->tm_q, c->tm_kv, a, st);
+      launch_attn(c, t->tm_q, c->tm_kv, a, st);
     }
   } else {  // O_PROJ / DOWN_PROJ: residual add (tensor parallel: partial sum + all-reduce)
     GemmParams p{};
@@ -756,6 +759,8 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   c->free_pages.resize(kv_pages);
   for (long long i = 0; i < kv_pages; ++i) c->free_pages[i] = (int)(kv_pages - 1 - i);
   CK(cudaMalloc(&c->ws, (size_t)8 * c->num_sms * kGemmBM * 256 * sizeof(float)));
+  CK(cudaMalloc(&c->attn_sched, 2 * sizeof(int)));
+  CK(cudaMemset(c->attn_sched, 0, 2 * sizeof(int)));
   CK(cudaMalloc(&c->tickets, 4096 * sizeof(int)));
   CK(cudaMemset(c->tickets, 0, 4096 * sizeof(int)));
   CK(cudaHostAlloc(&c->hctl, sizeof(HostCtl), cudaHostAllocMapped));
@@ -796,6 +801,7 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaFree(c->kv);
   cudaFree(c->ws);
   cudaFree(c->tickets);
+  cudaFree(c->attn_sched);
   cudaFree(c->gemm_dbg);
   cudaFreeHost((void*)c->hctl);
   for (void* ptr : c->tp_opened) cudaIpcCloseMemHandle(ptr);
