@@ -361,7 +361,7 @@ def run_ours(args):
     good = None
     if rank == 0 and not args.skip_goodput:
         try:
-            good = calibrated_goodput(prof, shape, args)
+            good = calibrated_goodput(prof, shape, args, ws)
         except Exception as e:  # keep the bench line even if the reference is unavailable
             good = {"error": repr(e)[:200]}
 
@@ -582,7 +582,7 @@ def live_check(ctx, shape, good, args):
     }
 
 
-def calibrated_goodput(prof, shape, args):
+def calibrated_goodput(prof, shape, args, n_instances: int = 1):
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.calibrate import fit_cost_params, predicted_vs_measured
 
@@ -614,6 +614,18 @@ def calibrated_goodput(prof, shape, args):
         out["edf_chunk2048_value"] = r2.value
     except Exception as e:
         out["edf_chunk2048_value"] = repr(e)[:120]
+    if n_instances > 1:
+        # the whole N-GPU deployment: round-robin proxy over N independent instances, the
+        # reference bisection over the merged outcomes (dispatch.goodput_search_instances)
+        from paper_2602_16603_b200 import dispatch
+
+        base_n = config2_trace(rate=20.0 * n_instances, duration=args.goodput_duration)
+        rd = dispatch.goodput_search_instances(base_n, rc, n_instances, target=0.9,
+                                               rate_bounds=(1.0, 512.0 * n_instances), tol=0.05)
+        out["deployment"] = {"instances": n_instances, "value": rd.value, "unit": "req/s",
+                             "saturated": rd.saturated, "probes": rd.num_runs,
+                             "method": "round-robin over independent instances, reference "
+                                       "goodput_search over the merged outcomes"}
     return out
 
 
