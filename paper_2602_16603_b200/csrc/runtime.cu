@@ -161,7 +161,7 @@ struct fp_ctx {
   int hq = 0, hkv = 0, ffn = 0;
   int qdim = 0, kvdim = 0, qkv_n = 0, vocab_pad = 0;
   int tp_rank = 0, tp_size = 1;
-  cudaStream_t stream = nullptr, upload = nullptr;
+  cudaStream_t stream = nullptr, upload = nullptr, readback = nullptr;
   cudaStream_t own_stream = nullptr;  // lock-step TP groups share rank 0's stream
   // tensor parallel exchange (null when tp_size == 1)
   TpDev tp_host{};
@@ -684,6 +684,7 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = c->stream;
   CK(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->readback, cudaStreamNonBlocking));
   // let the async mempool keep freed task workspaces
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -812,6 +813,7 @@ int fp_ctx_destroy(fp_ctx* c) {
   if (c->stage_ev) cudaEventDestroy(c->stage_ev);
   cudaStreamDestroy(c->own_stream);
   cudaStreamDestroy(c->upload);
+  cudaStreamDestroy(c->readback);
   delete c;
   return FP_OK;
 }
@@ -1385,9 +1387,13 @@ int fp_task_logits(fp_ctx* c, fp_task* task, float* host_out) {
   Task* t = reinterpret_cast<Task*>(task);
   REQ(c && t && host_out, "null argument");
   CK(cudaSetDevice(c->device));
-  CK(cudaStreamSynchronize(c->stream));
-  CK(cudaMemcpy2D(host_out, (size_t)c->cfg.vocab * 4, t->logits, (size_t)c->vocab_pad * 4,
-                  (size_t)c->cfg.vocab * 4, t->n_seqs, cudaMemcpyDeviceToHost));
+  // wait for THIS task only (its completion event), so a serving loop reads finished requests
+  // while later tasks still run on the prefill stream
+  if (t->done_recorded) CK(cudaEventSynchronize(t->done));
+  else CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy2DAsync(host_out, (size_t)c->cfg.vocab * 4, t->logits, (size_t)c->vocab_pad * 4,
+                       (size_t)c->cfg.vocab * 4, t->n_seqs, cudaMemcpyDeviceToHost, c->readback));
+  CK(cudaStreamSynchronize(c->readback));
   return FP_OK;
 }
 
