@@ -106,14 +106,27 @@ def gather_results(local_result, group=None) -> list:
     return bucket
 
 
+def _reference_run(args):
+    tr, pol, par, sd, ev = args
+    return refsim.load().run(tr, pol, par, sd, record_events=ev)
+
+
 def run_instances(trace, n_instances: int, policy, params, seed: int = 0, runner=None,
-                  record_events: bool = False) -> list:
+                  record_events: bool = False, jobs: int = 1) -> list:
     """Round-robin ``trace`` over n instances and run each (``runner(trace, policy, params,
-    seed, record_events)``; default: the reference ``run`` with whatever engine is injected)."""
-    ps = refsim.load()
-    runner = runner or (lambda tr, pol, par, sd, ev: ps.run(tr, pol, par, sd, record_events=ev))
-    return [runner(part, policy, params, seed, record_events)
-            for part in round_robin(trace, n_instances)]
+    seed, record_events)``; default: the reference ``run`` with whatever engine is injected).
+    ``jobs`` > 1 simulates the instances of the default runner in a process pool (virtual
+    clock only; results are identical to the serial run)."""
+    parts = round_robin(trace, n_instances)
+    if runner is None and jobs > 1 and n_instances > 1:
+        from concurrent.futures import ProcessPoolExecutor
+
+        with ProcessPoolExecutor(max_workers=min(jobs, n_instances)) as pool:
+            return list(pool.map(_reference_run,
+                                 [(p, policy, params, seed, record_events) for p in parts]))
+    if runner is None:
+        return [_reference_run((p, policy, params, seed, record_events)) for p in parts]
+    return [runner(part, policy, params, seed, record_events) for part in parts]
 
 
 def write_run_artifacts(results: Sequence, out_dir: str, config_hash: str | None = None) -> dict:
@@ -171,7 +184,8 @@ def sweep_instances(trace, n_instances: int, policy, params, rates: Sequence[flo
 
 
 def goodput_search_instances(trace, run_config, n_instances: int, target: float = 0.9,
-                             rate_bounds=(0.25, 16.0), tol: float = 0.05, runner=None):
+                             rate_bounds=(0.25, 16.0), tol: float = 0.05, runner=None,
+                             jobs: int = 1):
     """The reference's own goodput bisection (metrics.py:87-140) over the whole n-instance
     deployment: its per-probe ``run`` (resolved as a module global at call time) is swapped
     for round-robin dispatch + merge while the search runs."""
@@ -180,11 +194,9 @@ def goodput_search_instances(trace, run_config, n_instances: int, target: float 
 
     orig = M.run
 
-    base = runner or (lambda t, p, c, s, ev: orig(t, p, c, s, record_events=ev))
-
     def deployment_run(tr, policy, params, seed=0, record_events=False):
-        return merge_results(run_instances(tr, n_instances, policy, params, seed, base,
-                                           record_events))
+        return merge_results(run_instances(tr, n_instances, policy, params, seed, runner,
+                                           record_events, jobs))
 
     M.run = deployment_run
     try:
