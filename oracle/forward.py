@@ -15,7 +15,9 @@ timeline numerically, entry by entry, with the same semantics:
 * the stream is cut into ``chunk_size`` chunks, or one chunk when unchunked
   (cost_model.py:214-219);
 * entries run chunk -> layer -> operator in ``DENSE_LAYER_OPS`` order
-  ``qkv_proj, attn, o_proj, gate_up_proj, down_proj`` (cost_model.py:38-44, 224-242);
+  ``qkv_proj, attn, o_proj, gate_up_proj, down_proj`` (cost_model.py:38-44, 224-242), or
+  ``MOE_LAYER_OPS`` ``qkv_proj, attn, o_proj, gate, experts`` for MoE models
+  (cost_model.py:46-52; pinned to HF ``Qwen3MoeForCausalLM``);
 * linear operators act on all ``new_total`` tokens of the chunk (cost_model.py:225,236);
 * attention is per request: each request's share of the chunk attends causally to its own
   prefix + share and never across the batch (cost_model.py:226-233;
@@ -39,6 +41,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 OPS = ("qkv_proj", "attn", "o_proj", "gate_up_proj", "down_proj")
+MOE_OPS = ("qkv_proj", "attn", "o_proj", "gate", "experts")  # cost_model.py:46-52
 
 
 @dataclass(frozen=True)
@@ -54,6 +57,22 @@ class Shape:
     rms_eps: float = 1e-5
     qkv_bias: bool = False  # Qwen2.5: biases on q/k/v projections
     qk_norm: bool = False   # Qwen3: per-head RMSNorm of q and k before RoPE
+    # MoE (Qwen3-MoE block; every layer sparse): the FFN becomes a router ("gate" entry:
+    # softmax over experts, top-k, optional renormalisation) and the top-k SwiGLU experts
+    # ("experts" entry: weighted sum added to the residual)
+    n_experts: int = 0
+    top_k: int = 0
+    moe_ffn: int = 0
+    norm_topk: bool = False
+    router_std: float = 0.02
+
+    @property
+    def moe(self) -> bool:
+        return self.n_experts > 0
+
+    @property
+    def ops(self) -> tuple:
+        return MOE_OPS if self.moe else OPS
 
     @property
     def qdim(self) -> int:
@@ -75,6 +94,10 @@ SHAPES = {
     # tensor-parallel parity (config 4 family: Qwen2.5 QKV bias, GQA group 5 like Qwen2.5-32B;
     # TP=4 leaves 5 q heads / 1 kv head per rank and a padded 896-wide qkv shard)
     "tiny-qwen2-tp": Shape(4, 512, 20, 4, 128, 2048, 8000, 1e6, 1e-6, qkv_bias=True),
+    # MoE parity (Qwen3-MoE block: q/k-norm, 16 experts, top-4, renormalised; the router scale
+    # keeps the top-k margins far above bf16 rounding so routing is comparable exactly)
+    "tiny-moe": Shape(2, 512, 4, 2, 128, 0, 8000, 1e6, 1e-6, qk_norm=True, n_experts=16,
+                      top_k=4, moe_ffn=256, norm_topk=True, router_std=0.25),
 }
 
 
@@ -109,9 +132,17 @@ def make_weights(shape: Shape, seed: int, std: float = 0.02) -> dict:
         w[f"{l}.wk"] = normal(shape.kvdim, d)
         w[f"{l}.wv"] = normal(shape.kvdim, d)
         w[f"{l}.wo"] = normal(d, shape.qdim)
-        w[f"{l}.w_gate"] = normal(f, d)
-        w[f"{l}.w_up"] = normal(f, d)
-        w[f"{l}.w_down"] = normal(d, f)
+        if shape.moe:
+            E, I = shape.n_experts, shape.moe_ffn
+            w[f"{l}.w_router"] = bf16_round(
+                rng.standard_normal((E, d), dtype=np.float32) * shape.router_std)
+            w[f"{l}.e_gate"] = normal(E, I, d)
+            w[f"{l}.e_up"] = normal(E, I, d)
+            w[f"{l}.e_down"] = normal(E, d, I)
+        else:
+            w[f"{l}.w_gate"] = normal(f, d)
+            w[f"{l}.w_up"] = normal(f, d)
+            w[f"{l}.w_down"] = normal(d, f)
         w[f"{l}.attn_norm"] = gamma(d)
         w[f"{l}.ffn_norm"] = gamma(d)
         if shape.qkv_bias:
@@ -177,6 +208,33 @@ def causal_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_pos0: int) -
     p = np.exp(scores)
     p /= p.sum(axis=-1, keepdims=True)
     return np.einsum("hqk,khd->qhd", p, vr, optimize=True).astype(np.float32)
+
+
+def moe_route(xn: np.ndarray, w_router: np.ndarray, top_k: int, norm_topk: bool):
+    """Qwen3-MoE router: softmax over all experts (fp32), the top-k probabilities (ties to the
+    lower expert index), renormalised to sum 1 when ``norm_topk``. Returns ids [n, k] in
+    descending-probability order and their weights [n, k]."""
+    logits = (xn @ w_router.T).astype(np.float32)
+    z = logits - logits.max(axis=-1, keepdims=True)
+    p = np.exp(z)
+    p /= p.sum(axis=-1, keepdims=True)
+    order = np.lexsort((np.broadcast_to(np.arange(p.shape[1]), p.shape), -p), axis=-1)
+    ids = order[:, :top_k]
+    wts = np.take_along_axis(p, ids, axis=-1)
+    if norm_topk:
+        wts = wts / wts.sum(axis=-1, keepdims=True)
+    return ids.astype(np.int64), wts.astype(np.float32)
+
+
+def moe_experts(xn: np.ndarray, ids: np.ndarray, wts: np.ndarray, e_gate, e_up, e_down):
+    """sum_j w_j * down_e(silu(gate_e(x)) * up_e(x)) over the token's top-k experts."""
+    out = np.zeros_like(xn, dtype=np.float32)
+    for e in np.unique(ids):
+        tok, slot = np.nonzero(ids == e)
+        x = xn[tok]
+        y = (silu(x @ e_gate[e].T) * (x @ e_up[e].T)) @ e_down[e].T
+        out[tok] += wts[tok, slot][:, None] * y
+    return out
 
 
 # ----------------------------------------------------------------------------- plan
@@ -280,6 +338,11 @@ class OracleTask:
         per_chunk = self.shape.num_layers * len(OPS)
         return i // per_chunk, (i % per_chunk) // len(OPS), i % len(OPS)
 
+    # MoE routing of the current chunk (the live state between the gate and experts entries)
+    moe_ids: Optional[np.ndarray] = None
+    moe_w: Optional[np.ndarray] = None
+    xn: Optional[np.ndarray] = None
+
     def run(self, first: int, last: int) -> None:
         """Execute entries [first, last); first must equal the cursor (work conservation)."""
         if first != self.cursor:
@@ -337,11 +400,19 @@ class OracleTask:
             self.ao = ao.reshape(ch.new_total, sh.qdim)
         elif op == 2:  # o_proj + residual
             self.h = self.h + self.ao @ w[P + "wo"].T
+        elif op == 3 and sh.moe:  # gate: rmsnorm + router softmax + top-k
+            self.xn = rmsnorm(self.h, w[P + "ffn_norm"], sh.rms_eps)
+            self.moe_ids, self.moe_w = moe_route(self.xn, w[P + "w_router"], sh.top_k,
+                                                 sh.norm_topk)
         elif op == 3:  # rmsnorm + gate/up + SwiGLU
             xn = rmsnorm(self.h, w[P + "ffn_norm"], sh.rms_eps)
             self.act = silu(xn @ w[P + "w_gate"].T) * (xn @ w[P + "w_up"].T)
-        else:  # down_proj + residual (+ final norm and lm_head of completing requests)
-            self.h = self.h + self.act @ w[P + "w_down"].T
+        else:  # down_proj / experts + residual (+ final norm and lm_head of completing requests)
+            if sh.moe:
+                self.h = self.h + moe_experts(self.xn, self.moe_ids, self.moe_w,
+                                              w[P + "e_gate"], w[P + "e_up"], w[P + "e_down"])
+            else:
+                self.h = self.h + self.act @ w[P + "w_down"].T
             if layer == sh.num_layers - 1:
                 for req, row in ch.last:
                     xf = rmsnorm(self.h[row : row + 1], w["final_norm"], sh.rms_eps)

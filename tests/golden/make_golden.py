@@ -117,6 +117,59 @@ def hf_qwen_logits(shape: F.Shape, w: dict, tokens: list) -> np.ndarray:
     return np.stack(out).astype(np.float32)
 
 
+def hf_qwen3_moe_logits(shape: F.Shape, w: dict, tokens: list) -> np.ndarray:
+    """Last-token logits of HF ``Qwen3MoeForCausalLM`` (every layer sparse) in fp32."""
+    import torch
+    from transformers import Qwen3MoeConfig, Qwen3MoeForCausalLM
+
+    cfg = Qwen3MoeConfig(vocab_size=shape.vocab, hidden_size=shape.hidden,
+                         num_hidden_layers=shape.num_layers, num_attention_heads=shape.n_heads,
+                         num_key_value_heads=shape.n_kv_heads, head_dim=shape.head_dim,
+                         rope_theta=shape.rope_theta, rms_norm_eps=shape.rms_eps,
+                         num_experts=shape.n_experts, num_experts_per_tok=shape.top_k,
+                         moe_intermediate_size=shape.moe_ffn, norm_topk_prob=shape.norm_topk,
+                         decoder_sparse_step=1, mlp_only_layers=[], tie_word_embeddings=False,
+                         max_position_embeddings=65536, attn_implementation="eager")
+    model = Qwen3MoeForCausalLM(cfg).float().eval()
+    sd = {"model.embed_tokens.weight": w["embed"], "lm_head.weight": w["lm_head"],
+          "model.norm.weight": w["final_norm"]}
+    for l in range(shape.num_layers):
+        p = f"model.layers.{l}."
+        for hf, ours in (("self_attn.q_proj.weight", "wq"), ("self_attn.k_proj.weight", "wk"),
+                         ("self_attn.v_proj.weight", "wv"), ("self_attn.o_proj.weight", "wo"),
+                         ("self_attn.q_norm.weight", "q_norm"),
+                         ("self_attn.k_norm.weight", "k_norm"),
+                         ("input_layernorm.weight", "attn_norm"),
+                         ("post_attention_layernorm.weight", "ffn_norm"),
+                         ("mlp.gate.weight", "w_router"), ("mlp.experts.down_proj", "e_down")):
+            sd[p + hf] = w[f"{l}.{ours}"]
+        sd[p + "mlp.experts.gate_up_proj"] = np.concatenate([w[f"{l}.e_gate"], w[f"{l}.e_up"]],
+                                                            axis=1)
+    missing = {m for m in set(model.state_dict()) - set(sd) if "rotary" not in m}
+    assert not missing, missing
+    model.load_state_dict({k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in sd.items()},
+                          strict=False)
+    out = []
+    with torch.no_grad():
+        for t in tokens:
+            ids = torch.from_numpy(t.astype(np.int64))[None]
+            out.append(model(input_ids=ids).logits[0, -1].numpy())
+    return np.stack(out).astype(np.float32)
+
+
+def moe_golden() -> None:
+    sh = F.SHAPES["tiny-moe"]
+    w = F.make_weights(sh, TINY_SEED)
+    toks = F.make_tokens(TINY_LENS, sh.vocab, TINY_SEED)
+    ref = hf_qwen3_moe_logits(sh, w, toks)
+    ours = F.forward_logits(sh, w, toks)
+    err = np.abs(ours - ref).max()
+    print("oracle vs HF tiny-moe: max abs err", err, "max |logit|", np.abs(ref).max())
+    assert err < 1e-3, err
+    np.savez_compressed(os.path.join(HERE, "tiny-moe_hf_logits.npz"), seed=TINY_SEED,
+                        lens=np.array(TINY_LENS), logits=ref)
+
+
 def reference_events() -> None:
     for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
         if os.path.isdir(os.path.join(p, "prefillsim")):
@@ -167,4 +220,8 @@ def main() -> None:
 
 
 if __name__ == "__main__":
-    main()
+    if "--moe" in sys.argv:
+        moe_golden()
+    else:
+        main()
+        moe_golden()

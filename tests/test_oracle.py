@@ -104,3 +104,24 @@ def test_oracle_matches_hf_qwen_goldens(golden_dir, name):
     w = F.make_weights(shape, int(g["seed"]))
     tokens = F.make_tokens(list(g["lens"]), shape.vocab, int(g["seed"]))
     np.testing.assert_allclose(F.forward_logits(shape, w, tokens), g["logits"], rtol=0, atol=1e-4)
+
+
+def test_oracle_matches_hf_qwen3_moe_golden(golden_dir):
+    """MoE layers (router softmax + top-k + renormalised SwiGLU experts, cost_model.py:46-52)
+    pinned to HF Qwen3MoeForCausalLM."""
+    g = np.load(os.path.join(golden_dir, "tiny-moe_hf_logits.npz"))
+    shape = F.SHAPES["tiny-moe"]
+    w = F.make_weights(shape, int(g["seed"]))
+    tokens = F.make_tokens(list(g["lens"]), shape.vocab, int(g["seed"]))
+    np.testing.assert_allclose(F.forward_logits(shape, w, tokens), g["logits"], rtol=0, atol=1e-4)
+    # chunked and preempted execution give the same logits (routing is per token)
+    np.testing.assert_allclose(F.forward_logits(shape, w, tokens, chunk_size=100), g["logits"],
+                               rtol=0, atol=1e-4)
+
+
+def test_moe_route_ties_and_renorm():
+    xn = np.eye(4, dtype=np.float32)
+    wr = np.array([[1, 0, 0, 0], [1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 0]], np.float32)
+    ids, wts = F.moe_route(xn, wr, 2, True)
+    assert ids[0].tolist() == [0, 1]            # tie between experts 0 and 1: lower index first
+    np.testing.assert_allclose(wts.sum(-1), 1.0, rtol=1e-6)
