@@ -39,6 +39,9 @@ extern "C" {
 #define FP_OP_O_PROJ 2
 #define FP_OP_GATE_UP_PROJ 3
 #define FP_OP_DOWN_PROJ 4
+/* MoE layers (n_experts > 0) replace the last two: prefillsim/cost_model.py:46-52. */
+#define FP_OP_GATE 3    /* router: fused post-attention norm, logits GEMM, softmax top-k, dispatch */
+#define FP_OP_EXPERTS 4 /* grouped expert gate/up + SwiGLU, grouped down, weighted combine */
 
 /* Weight tensor ids for fp_weights_load (canonical, unpacked Llama layout, bf16 row-major). */
 #define FP_W_EMBED 0      /* [vocab, hidden] */
@@ -58,6 +61,10 @@ extern "C" {
 #define FP_W_V_BIAS 14    /* [n_kv_heads*head_dim] */
 #define FP_W_Q_NORM 15    /* [head_dim]              (Qwen3: qk_norm) */
 #define FP_W_K_NORM 16    /* [head_dim] */
+#define FP_W_ROUTER 17       /* [n_experts, hidden]                    (MoE) */
+#define FP_W_EXPERT_GATE 18  /* [n_experts, moe_ffn, hidden] */
+#define FP_W_EXPERT_UP 19    /* [n_experts, moe_ffn, hidden] */
+#define FP_W_EXPERT_DOWN 20  /* [n_experts, hidden, moe_ffn] */
 
 typedef struct fp_model_cfg {
   int32_t num_layers; /* CostParams.num_layers, cost_model.py:92 */
@@ -72,6 +79,11 @@ typedef struct fp_model_cfg {
   float rms_eps;
   int32_t qkv_bias; /* 1: q/k/v projections carry a bias (Qwen2.5) */
   int32_t qk_norm;  /* 1: per-head RMSNorm of q and k before RoPE (Qwen3) */
+  /* MoE (Qwen3-MoE block, every layer sparse; n_experts = 0: dense). ffn is unused then. */
+  int32_t n_experts;  /* <= 256 */
+  int32_t top_k;      /* <= 16 */
+  int32_t moe_ffn;    /* expert intermediate size, multiple of 128 */
+  int32_t norm_topk;  /* 1: renormalise the top-k router probabilities to sum 1 */
 } fp_model_cfg;
 
 typedef struct fp_ctx fp_ctx;
@@ -159,6 +171,10 @@ int fp_poll(fp_ctx* ctx, fp_status* out);
 
 /* ---- parity taps ----------------------------------------------------------------------- */
 int fp_task_logits(fp_ctx* ctx, fp_task* task, float* host_out); /* [n_seqs, vocab] */
+/* MoE parity tap: routing of the most recent gate entry (its chunk's rows): expert ids and
+ * weights [chunk_tokens, top_k], descending probability. */
+int fp_task_read_routing(fp_ctx* ctx, fp_task* task, int32_t* host_ids, float* host_w,
+                         int32_t max_rows);
 int fp_task_read_kv(fp_ctx* ctx, fp_task* task, int32_t seq, int32_t layer, void* host_k,
                     void* host_v); /* each [seq_len, n_kv_heads, head_dim] bf16 */
 
@@ -172,6 +188,11 @@ int fp_task_read_kv(fp_ctx* ctx, fp_task* task, int32_t seq, int32_t layer, void
 #define FP_K_LM_HEAD 6
 #define FP_K_RMS_FINAL 7
 #define FP_K_XCHG 8 /* tensor-parallel all-reduce of o_proj / down_proj partials */
+#define FP_K_ROUTER 9        /* MoE router logits GEMM */
+#define FP_K_MOE_DISPATCH 10 /* top-k routing, expert offsets, row gather */
+#define FP_K_EXPERT_GU 11    /* grouped expert gate/up + SwiGLU GEMM */
+#define FP_K_EXPERT_DOWN 12  /* grouped expert down GEMM */
+#define FP_K_MOE_COMBINE 13  /* weighted combine into the residual */
 typedef struct fp_prof_rec {
   int32_t kind;  /* FP_K_* */
   int32_t layer;

@@ -23,6 +23,7 @@ FP_TASK_IDLE, FP_TASK_RUNNING, FP_TASK_STOPPED, FP_TASK_DONE = 0, 1, 2, 3
 W_EMBED, W_Q, W_K, W_V, W_O, W_GATE, W_UP, W_DOWN = range(8)
 W_ATTN_NORM, W_FFN_NORM, W_FINAL_NORM, W_LM_HEAD = 8, 9, 10, 11
 W_Q_BIAS, W_K_BIAS, W_V_BIAS, W_Q_NORM, W_K_NORM = 12, 13, 14, 15, 16
+W_ROUTER, W_EXPERT_GATE, W_EXPERT_UP, W_EXPERT_DOWN = 17, 18, 19, 20
 
 
 class NativeError(RuntimeError):
@@ -43,6 +44,10 @@ class ModelCfg(C.Structure):
         ("rms_eps", C.c_float),
         ("qkv_bias", C.c_int32),
         ("qk_norm", C.c_int32),
+        ("n_experts", C.c_int32),
+        ("top_k", C.c_int32),
+        ("moe_ffn", C.c_int32),
+        ("norm_topk", C.c_int32),
     ]
 
 
@@ -92,7 +97,8 @@ class ProfRec(C.Structure):
 
 
 KERNEL_KINDS = ("rmsnorm", "qkv_gemm", "attn", "o_gemm", "gate_up_gemm", "down_gemm",
-                "lm_head_gemm", "final_rmsnorm", "tp_allreduce")
+                "lm_head_gemm", "final_rmsnorm", "tp_allreduce", "router_gemm", "moe_dispatch",
+                "expert_gate_up_gemm", "expert_down_gemm", "moe_combine")
 
 
 class TpHandle(C.Structure):
@@ -117,6 +123,7 @@ _SIGS = {
     "fp_ctx_free_pages": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "fp_ctx_set_window": (C.c_int, [_P, _I]),
     "fp_ctx_set_gemm_policy": (C.c_int, [_P, _I, _I]),
+    "fp_task_read_routing": (C.c_int, [_P, _P, _P, _P, _I]),
     "fp_debug_gemm_stamps": (C.c_int, [_P, _P, _I]),
     "fp_sync": (C.c_int, [_P]),
     "fp_weights_init_random": (C.c_int, [_P, C.c_uint64, C.c_float]),

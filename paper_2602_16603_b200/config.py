@@ -19,6 +19,15 @@ class ModelShape:
     rms_eps: float = 1e-5
     qkv_bias: bool = False  # Qwen2.5
     qk_norm: bool = False   # Qwen3
+    # MoE (Qwen3-MoE: every layer's FFN is a router + top-k SwiGLU experts; ffn unused)
+    n_experts: int = 0
+    top_k: int = 0
+    moe_ffn: int = 0
+    norm_topk: bool = False
+
+    @property
+    def moe(self) -> bool:
+        return self.n_experts > 0
 
     @property
     def qdim(self) -> int:
@@ -31,7 +40,11 @@ class ModelShape:
     def gemm_flops_per_token(self) -> float:
         """2 * (qkv + o + gate_up + down) weights, per token per layer."""
         d = self.hidden
-        w = d * (self.qdim + 2 * self.kvdim) + self.qdim * d + 2 * d * self.ffn + self.ffn * d
+        if self.moe:  # router + the top_k active experts
+            ffn = self.n_experts * d + self.top_k * 3 * d * self.moe_ffn
+        else:
+            ffn = 3 * d * self.ffn
+        w = d * (self.qdim + 2 * self.kvdim) + self.qdim * d + ffn
         return 2.0 * w
 
     def attn_flops(self, share: int, prefix: int) -> float:
@@ -59,4 +72,10 @@ SHAPES = {
                              qkv_bias=True),
     "tiny-qwen2-tp": ModelShape("tiny-qwen2-tp", 4, 512, 20, 4, 128, 2048, 8000, 1e6, 1e-6,
                                 qkv_bias=True),
+    # MoE: Qwen3-30B-A3B shape (128 experts, top-8, expert ffn 768)
+    "qwen3-30b-a3b": ModelShape("qwen3-30b-a3b", 48, 2048, 32, 4, 128, 0, 151936, 1e6, 1e-6,
+                                qk_norm=True, n_experts=128, top_k=8, moe_ffn=768,
+                                norm_topk=True),
+    "tiny-moe": ModelShape("tiny-moe", 2, 512, 4, 2, 128, 0, 8000, 1e6, 1e-6, qk_norm=True,
+                           n_experts=16, top_k=4, moe_ffn=256, norm_topk=True),
 }

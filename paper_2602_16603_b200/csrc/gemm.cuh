@@ -68,6 +68,12 @@ struct GemmParams {
   const float* ssq_in;
   float* ssq_out;
   unsigned long long* dbg;  // phase stamps (%globaltimer ns) [cta][16] for diagnostics, or null
+  // MODE 2 (grouped MoE experts)
+  const int* grp_mtiles;  // [m-tiles] int2 (expert, first A row)
+  const int* grp_count;   // number of m-tiles
+  const int* grp_off;     // [E + 1] expert row offsets (live-row bound)
+  const int* grp_perm;    // [rows] token of each row (fused-norm lookup)
+  int grp_b_rows;         // B rows per expert
   Guard guard;
 };
 
@@ -214,7 +220,8 @@ __device__ __noinline__ void split_item_epilogue(const GemmParams& p, const Gmem
   constexpr int BN = 256;
   const int lane = threadIdx.x & 31;
   float rs = 1.f;  // fused input RMSNorm factor of the row
-  if ((EPI == EPI_QKV || EPI == EPI_SWIGLU) && p.ssq_in != nullptr && valid) {
+  if ((EPI == EPI_QKV || EPI == EPI_SWIGLU || EPI == EPI_STORE_F32) && p.ssq_in != nullptr &&
+      valid) {
     const float* sp = p.ssq_in + (long long)m * p.nseg;
     float ssum = 0.f;
     for (int i = 0; i < p.nseg; ++i) ssum += __ldg(sp + i);
@@ -254,6 +261,8 @@ __device__ __noinline__ void split_item_epilogue(const GemmParams& p, const Gmem
     if (!valid) return;
     sum.get(r, g * 32, g * 32 + 16, v);
     if constexpr (EPI == EPI_STORE_F32) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= rs;  // fused norm (MoE router logits)
       float* dst = reinterpret_cast<float*>(p.out) + (long long)m * p.ldo + n0 + g * 32;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -346,9 +355,13 @@ __device__ __noinline__ void split_item_epilogue(const GemmParams& p, const Gmem
   }
 }
 
-// SPLIT: the instantiation that also runs tail split-K tiles (launched only when the launcher
-// chose splits > 1; the unsplit instantiation carries no split code and no extra registers).
-template <int BN, int EPI, int CG, bool SPLIT>
+// MODE 0: plain tiles. MODE 1: the instantiation that also runs tail split-K tiles (launched only
+// when the launcher chose splits > 1; MODE 0 carries no split code and no extra registers).
+// MODE 2: grouped GEMM for MoE experts -- A rows are expert-ordered segments, the m-tile table
+// (expert, first row) and its length come from device memory (moe_plan_kernel), the B rows of
+// expert e start at e * grp_b_rows, rows past the expert's segment are masked, and the fused
+// norm looks up each row's token through grp_perm. CG = 1 only.
+template <int BN, int EPI, int CG, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
@@ -401,7 +414,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const bool run = guard_block(p.guard);
   if (threadIdx.x == 0) GEMM_STAMP(2);
 
-  const int num_m = (p.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
+  const int num_m = MODE == 2 ? (run ? *p.grp_count : 0) : (p.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
   const int unit0 = blockIdx.x / CG;      // this CTA (pair)'s first work unit
   const int unit_step = gridDim.x / CG;
   const int num_n = p.N / BN;
@@ -428,6 +441,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       kb1 = min(num_k, kb0 + per);
     }
   };
+  // tile -> (m-block, n-block, first A row, first B row, end of live rows)
+  auto tile_geom = [&](int tile, int& mb, int& nb, int& row_a, int& row_b, int& row_end) {
+    if constexpr (MODE == 2) {
+      int mt;
+      tile_coords(tile, num_m, num_n, mt, nb);
+      const int2 te = reinterpret_cast<const int2*>(p.grp_mtiles)[mt];
+      mb = mt;
+      row_a = te.y;
+      row_b = te.x * p.grp_b_rows + nb * BN;
+      row_end = p.grp_off[te.x + 1];
+    } else {
+      tile_coords(tile, num_m, num_n, mb, nb);
+      row_a = mb * Cfg::TILE_M + (int)rank * kGemmBM;
+      row_b = nb * BN + (int)rank * (BN / CG);
+      row_end = p.M;
+    }
+  };
 
   if (warp == 0) {
     const uint64_t pol_b = policy_evict_last();
@@ -436,10 +466,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int u = unit0; u < num_units; u += unit_step) {
       int tile, split, nsplit, kb0, kb1;
       unit_info(u, tile, split, nsplit, kb0, kb1);
-      int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
-      const int row_a = mb * Cfg::TILE_M + (int)rank * kGemmBM;
-      const int row_b = nb * BN + (int)rank * (BN / CG);
+      int mb, nb, row_a, row_b, row_end;
+      tile_geom(tile, mb, nb, row_a, row_b, row_end);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[s], ph ^ 1);
         if (lane == 0) {
@@ -526,12 +554,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int u = unit0; u < num_units; u += unit_step, ++it) {
       int tile, split, splits, kb0, kb1;
       unit_info(u, tile, split, splits, kb0, kb1);
-      int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      int mb, nb, row_a, row_b, row_end;
+      tile_geom(tile, mb, nb, row_a, row_b, row_end);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
-      const int m = mb * Cfg::TILE_M + (int)rank * kGemmBM + row;
-      const bool live = m < p.M;
+      const int m = row_a + row;
+      const bool live = m < row_end;
       const int n0 = nb * BN;
       // Partial tiles are stored thread-major ([split][col/4][row] float4) so every warp
       // access is one contiguous 512-byte segment.
@@ -539,7 +567,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       float4* ws_tile =
           reinterpret_cast<float4*>(p.ws) + (long long)wtile * splits * (BN / 4) * kGemmBM;
       const uint32_t tacc = tbase + acc * BN + ((uint32_t)(q * 32) << 16);
-      if (SPLIT && splits > 1) {
+      if (MODE == 1 && splits > 1) {
         mbar_wait(&tfull[acc], acc_ph);
         if (threadIdx.x == 128) GEMM_STAMP(6);
         tc_fence_after();
@@ -568,7 +596,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // 3) this K-slice's share of the tile's (row, column-group) epilogue items, each the
         //    split-order sum of the partials (deterministic) -- the reduction is spread over
         //    all K-slice CTAs instead of one CTA reducing the whole tile
-        const int m_base = mb * Cfg::TILE_M + (int)rank * kGemmBM;
+        const int m_base = row_a;
         const int live_rows = min(kGemmBM, p.M - m_base);
         const GmemSum gsum{ws_tile, splits};
         // 8 items per row, row-major: a warp covers 4 whole rows
@@ -590,8 +618,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // Unsplit tile: accumulator columns [col, col+32) of this thread's row from TMEM.
       // fused RMSNorm: the row's rsqrt factor (1 for epilogues without a norm in front)
       float rs = 1.f;
-      if ((EPI == EPI_QKV || EPI == EPI_SWIGLU) && p.ssq_in != nullptr && live) {
-        const float* sp = p.ssq_in + (long long)m * p.nseg;
+      if ((EPI == EPI_QKV || EPI == EPI_SWIGLU || EPI == EPI_STORE_F32) && p.ssq_in != nullptr &&
+          live) {
+        const int tok = MODE == 2 ? p.grp_perm[m] : m;
+        const float* sp = p.ssq_in + (long long)tok * p.nseg;
         float ssum = 0.f;
         for (int i = 0; i < p.nseg; ++i) ssum += __ldg(sp + i);
         rs = rsqrtf(ssum / (float)(p.nseg * 256) + p.norm_eps_in);

@@ -1,0 +1,221 @@
+// MoE routing, dispatch and combine kernels (Qwen3-MoE block) around the grouped expert GEMMs.
+//
+// Realises the reference's MoE operator pair (prefillsim/cost_model.py:46-52): `gate` and
+// `experts` replace gate_up_proj / down_proj in every layer of an `arch = "moe"` model, and stay
+// one preemption point each. Semantics follow Qwen3MoeSparseMoeBlock (HF transformers):
+// probabilities = softmax over all experts of the router logits (fp32), the top-k of them
+// (ties to the lower expert index), renormalised to sum 1 when norm_topk_prob, and the block
+// output is sum_j w_j * expert_{e_j}(x).
+//
+// gate entry:    router GEMM (tcgen05, fused post-attention norm, fp32 logits)
+//                -> moe_route_kernel   softmax / top-k per token, expert histogram
+//                -> moe_plan_kernel    expert row offsets (exclusive scan) + the m-tile table of
+//                                      the grouped GEMMs
+//                -> moe_scatter_kernel token rows gathered into expert-contiguous order
+// experts entry: grouped gate/up + SwiGLU GEMM -> grouped down GEMM (gemm.cuh MODE 2)
+//                -> moe_combine_kernel h += sum_j w_j y_j (j order: deterministic), and the
+//                                      next norm's segment sums of squares
+// A row's position inside its expert's segment depends on atomic order, but every GEMM output
+// row depends only on its own input row, so results are bit-identical run to run.
+#pragma once
+#include "common.cuh"
+#include "control.cuh"
+
+namespace fp {
+
+constexpr int kMoeMaxExperts = 256;
+constexpr int kMoeMaxTopK = 16;
+
+struct MoeParams {
+  int M;             // token rows of the chunk
+  int n_experts, top_k, norm_topk;
+  int d;             // hidden
+  const float* logits;   // [M, 256] router logits (gate entry)
+  int ld_logits;
+  int* topk_ids;         // [M, top_k]
+  float* topk_w;         // [M, top_k]
+  int* slot;             // [M, top_k] row of (token, j) in the expert-ordered buffers
+  int* counts;           // [E] histogram (zero between gate entries)
+  int* cursor;           // [E] scatter cursors (zero between gate entries)
+  int* offsets;          // [E + 1] expert row offsets
+  int* mtile_count;      // number of 128-row m-tiles of the grouped GEMMs
+  int2* mtiles;          // [max_mtiles] (expert, first row)
+  int* perm_tok;         // [M * top_k] token of each expert-ordered row
+  const __nv_bfloat16* h;  // residual stream [M, d] (scatter source, combine target)
+  __nv_bfloat16* h_out;
+  __nv_bfloat16* xperm;  // [M * top_k, d] gathered rows
+  const __nv_bfloat16* yperm;  // [M * top_k, d] expert outputs
+  float* ssq;            // [M, d / 256] segment sums of squares of the new h
+  Guard guard;
+};
+
+// One warp per token: softmax over the experts, top-k by repeated warp argmax.
+__global__ void __launch_bounds__(256) moe_route_kernel(const MoeParams p) {
+  grid_dep_wait();
+  if (!guard_block(p.guard)) return;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= p.M) return;
+  constexpr int PER = kMoeMaxExperts / 32;
+  float v[PER];
+  const float* lg = p.logits + (long long)t * p.ld_logits;
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < p.n_experts ? lg[e] : -INFINITY;
+    mx = fmaxf(mx, v[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    v[i] = lane + 32 * i < p.n_experts ? expf(v[i] - mx) : 0.f;
+    sum += v[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float inv = 1.f / sum;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) v[i] *= inv;  // probabilities; taken ones become -1
+  float wsel[kMoeMaxTopK];
+  int isel[kMoeMaxTopK];
+  float wsum = 0.f;
+  for (int j = 0; j < p.top_k; ++j) {
+    float bv = -1.f;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      if (v[i] > bv) {  // strict: within a lane the lower index wins ties
+        bv = v[i];
+        bi = lane + 32 * i;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((bi & 31) == lane) v[bi >> 5] = -1.f;
+    wsel[j] = bv;
+    isel[j] = bi;
+    wsum += bv;
+  }
+  if (lane == 0) {
+    const float norm = p.norm_topk ? 1.f / wsum : 1.f;
+    for (int j = 0; j < p.top_k; ++j) {
+      p.topk_ids[t * p.top_k + j] = isel[j];
+      p.topk_w[t * p.top_k + j] = wsel[j] * norm;
+      atomicAdd(&p.counts[isel[j]], 1);
+    }
+  }
+}
+
+// One CTA: expert offsets (exclusive scan of the histogram) and the grouped GEMMs' m-tile
+// table; re-arms the histogram and the scatter cursors.
+__global__ void __launch_bounds__(kMoeMaxExperts) moe_plan_kernel(const MoeParams p) {
+  __shared__ int s_cnt[kMoeMaxExperts], s_off[kMoeMaxExperts + 1], s_tiles[kMoeMaxExperts + 1];
+  grid_dep_wait();
+  if (!guard_block(p.guard)) return;
+  const int e = threadIdx.x;
+  const int cnt = e < p.n_experts ? p.counts[e] : 0;
+  s_cnt[e] = cnt;
+  __syncthreads();
+  if (e == 0) {
+    int o = 0, t = 0;
+    for (int i = 0; i < p.n_experts; ++i) {
+      s_off[i] = o;
+      s_tiles[i] = t;
+      o += s_cnt[i];
+      t += (s_cnt[i] + 127) / 128;
+    }
+    s_off[p.n_experts] = o;
+    s_tiles[p.n_experts] = t;
+    *p.mtile_count = t;
+  }
+  __syncthreads();
+  if (e < p.n_experts) p.offsets[e] = s_off[e];
+  if (e == 0) p.offsets[p.n_experts] = s_off[p.n_experts];
+  if (e < p.n_experts) {
+    for (int k = 0; k < (cnt + 127) / 128; ++k) p.mtiles[s_tiles[e] + k] = make_int2(e, s_off[e] + 128 * k);
+    p.counts[e] = 0;
+    p.cursor[e] = 0;
+  }
+}
+
+// One warp per token: claim a row in each chosen expert's segment and copy the token's h row.
+__global__ void __launch_bounds__(256) moe_scatter_kernel(const MoeParams p) {
+  grid_dep_wait();
+  if (!guard_block(p.guard)) return;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= p.M) return;
+  const uint4* src = reinterpret_cast<const uint4*>(p.h + (long long)t * p.d);
+  const int vecs = p.d / 8;
+  for (int j = 0; j < p.top_k; ++j) {
+    int row = 0;
+    if (lane == 0) {
+      const int e = p.topk_ids[t * p.top_k + j];
+      row = p.offsets[e] + atomicAdd(&p.cursor[e], 1);
+      p.slot[t * p.top_k + j] = row;
+      p.perm_tok[row] = t;
+    }
+    row = __shfl_sync(0xffffffffu, row, 0);
+    uint4* dst = reinterpret_cast<uint4*>(p.xperm + (long long)row * p.d);
+    for (int i = lane; i < vecs; i += 32) dst[i] = ld_nc_v4(src + i);
+  }
+}
+
+// One warp per (token, 256-column segment): h += sum_j w_j * y[slot_j] (fp32, j order), and
+// the segment's sum of squares of the new (bf16-rounded) h for the next fused norm.
+__global__ void __launch_bounds__(256) moe_combine_kernel(const MoeParams p) {
+  grid_dep_wait();
+  if (!guard_block(p.guard)) return;
+  const int lane = threadIdx.x & 31;
+  const int nseg = p.d / 256;
+  const long long u = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (u >= (long long)p.M * nseg) return;
+  const int t = (int)(u / nseg), sg = (int)(u - (long long)t * nseg);
+  const int c = sg * 256 + lane * 8;
+  float acc[8];
+  {
+    const uint4 hv = ld_global_v4(p.h + (long long)t * p.d + c);
+    const uint32_t w4[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = unpack_bf16x2(w4[i]);
+      acc[2 * i] = f.x;
+      acc[2 * i + 1] = f.y;
+    }
+  }
+  float y[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int j = 0; j < p.top_k; ++j) {
+    const float wj = p.topk_w[t * p.top_k + j];
+    const uint4 yv = ld_global_v4(p.yperm + (long long)p.slot[t * p.top_k + j] * p.d + c);
+    const uint32_t w4[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = unpack_bf16x2(w4[i]);
+      y[2 * i] += wj * f.x;
+      y[2 * i + 1] += wj * f.y;
+    }
+  }
+  float ss = 0.f;
+  uint32_t o4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o4[i] = pack_bf16x2(acc[2 * i] + y[2 * i], acc[2 * i + 1] + y[2 * i + 1]);
+    const float2 f = unpack_bf16x2(o4[i]);
+    ss += f.x * f.x + f.y * f.y;
+  }
+  st_global_v4(p.h_out + (long long)t * p.d + c, make_uint4(o4[0], o4[1], o4[2], o4[3]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0 && p.ssq) p.ssq[(long long)t * nseg + sg] = ss;
+}
+
+}  // namespace fp

@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "control.cuh"
 #include "gemm.cuh"
+#include "moe.cuh"
 #include "norm.cuh"
 #include "xchg.cuh"
 
@@ -120,6 +121,10 @@ struct Layer {
   float* bqkv = nullptr;                           // [qkv_n] (qkv_bias models)
   float *q_norm = nullptr, *k_norm = nullptr;      // [128]  (qk_norm models)
   CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
+  // MoE: router [256 (padded experts), d] and expert weights, post-attention norm folded into
+  // the router and gate/up columns; gate/up interleaved in 128-row blocks per expert
+  __nv_bfloat16 *wr = nullptr, *egu = nullptr, *ed = nullptr;
+  CUtensorMap tm_r, tm_egu, tm_ed;
 };
 
 struct ChunkPlan {
@@ -147,6 +152,15 @@ struct Task {
   float* logits;
   TaskCtl* ctl;
   CUtensorMap tm_h, tm_ao, tm_act, tm_xf, tm_q;
+  // MoE routing state of the current chunk (gate -> experts) and expert-ordered buffers
+  float* rlog = nullptr;                       // [max_m, 256] router logits
+  char* moe_meta = nullptr;                    // one allocation for the index arrays below
+  int *m_ids, *m_slot, *m_counts, *m_cursor, *m_off, *m_mtc, *m_perm;
+  float* m_w;
+  int2* m_mtiles;
+  __nv_bfloat16 *xperm = nullptr, *actp = nullptr, *yperm = nullptr;
+  CUtensorMap tm_xperm, tm_actp;
+  int moe_rows = 0;                            // rows of the current chunk's routing
   cudaEvent_t ready, done;
   // host execution state
   int gen = 0, seg_first = 0, enq = 0, seg_ack0 = 0, done_recorded = 0;
@@ -321,7 +335,7 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   using Cfg = GemmCfg<BN, CG>;
   static bool attr = false;
   if (!attr) {
-    for (auto k : {gemm_bf16_tn_kernel<BN, EPI, CG, false>, gemm_bf16_tn_kernel<BN, EPI, CG, true>}) {
+    for (auto k : {gemm_bf16_tn_kernel<BN, EPI, CG, 0>, gemm_bf16_tn_kernel<BN, EPI, CG, 1>}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
       if (CG == 2) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     }
@@ -365,8 +379,24 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
-  if (p.splits > 1) cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, true>, a, b, p);
-  else cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, false>, a, b, p);
+  if (p.splits > 1) cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 1>, a, b, p);
+  else cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 0>, a, b, p);
+}
+
+// Grouped (MoE expert) GEMM: persistent over the device-side m-tile table (gemm.cuh MODE 2).
+template <int EPI>
+static void launch_gemm_grouped(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
+                                GemmParams p, cudaStream_t st) {
+  using Cfg = GemmCfg<256, 1>;
+  auto kern = gemm_bf16_tn_kernel<256, EPI, 1, 2>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    attr = true;
+  }
+  p.splits = 1;
+  p.full_tiles = 0;
+  launch_pdl(kern, dim3(c->num_sms), dim3(kGemmThreads), Cfg::SMEM_BYTES, st, a, b, p);
 }
 
 // Pair (2-CTA, 256-row) tiles or single-CTA (128-row) tiles, whichever the cost model
@@ -431,6 +461,140 @@ static bool boundary_eligible(const fp_ctx* c, int gran, int i, int n_entries) {
 // anything after it (phase 2); a lock-step group on one device launches phase 1 of every rank
 // before phase 2 of any rank so no all-reduce waits on a kernel queued behind it.
 constexpr int kPhasePre = 1, kPhasePost = 2, kPhaseAll = 3;
+// Completion of the chunk's requests after the last layer: final norm + lm_head of their last
+// tokens (cost_model.py:240-241 charges this to the chunk).
+static int launch_final(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, const Guard& g2,
+                        cudaStream_t st) {
+  const fp_model_cfg& m = c->cfg;
+  if (ch.n_last == 0) return FP_OK;
+  RmsParams r{};
+  r.M = ch.n_last;
+  r.d = m.hidden;
+  r.src = t->h;
+  r.ld_src = m.hidden;
+  r.rows = t->d_last + ch.last0;
+  r.gamma = c->final_g;
+  r.out = t->xf;
+  r.ld_out = m.hidden;
+  r.eps = m.rms_eps;
+  r.guard = g2;
+  {
+    ProfScope ps(c, st, FP_K_RMS_FINAL, layer, ch.n_last, 0.0, 2.0 * ch.n_last * m.hidden * 2);
+    int rc = launch_rms(r, st);
+    if (rc) return rc;
+  }
+  GemmParams q{};
+  q.M = ch.n_last;
+  q.N = c->vocab_pad;
+  q.K = m.hidden;
+  q.out = t->logits + (long long)ch.seq0 * c->vocab_pad;
+  q.ldo = c->vocab_pad;
+  q.guard = g2;
+  ProfScope ps(c, st, FP_K_LM_HEAD, layer, ch.n_last, 2.0 * ch.n_last * q.N * q.K, 0.0);
+  launch_gemm<EPI_STORE_F32>(c, t->tm_xf, c->tm_lm, q, st);
+  return FP_OK;
+}
+
+// MoE layer, entries `gate` (op 3) and `experts` (op 4): moe.cuh. The post-attention norm is
+// fused into the router and the expert gate/up GEMM (folded weights + the row's rsqrt from the
+// segment sums of squares the o_proj epilogue wrote), exactly as for the dense gate_up_proj.
+static int launch_moe_entry(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, int op,
+                            const Guard& g, const Guard& g2, cudaStream_t st) {
+  const fp_model_cfg& m = c->cfg;
+  const int M = ch.M, d = m.hidden, E = m.n_experts, K = m.top_k, I = m.moe_ffn;
+  Layer& ly = c->layers[layer];
+  MoeParams mp{};
+  mp.M = M;
+  mp.n_experts = E;
+  mp.top_k = K;
+  mp.norm_topk = m.norm_topk;
+  mp.d = d;
+  mp.logits = t->rlog;
+  mp.ld_logits = 256;
+  mp.topk_ids = t->m_ids;
+  mp.topk_w = t->m_w;
+  mp.slot = t->m_slot;
+  mp.counts = t->m_counts;
+  mp.cursor = t->m_cursor;
+  mp.offsets = t->m_off;
+  mp.mtile_count = t->m_mtc;
+  mp.mtiles = t->m_mtiles;
+  mp.perm_tok = t->m_perm;
+  mp.h = t->h;
+  mp.h_out = t->h;
+  mp.xperm = t->xperm;
+  mp.yperm = t->yperm;
+  mp.ssq = t->ssq;
+  mp.guard = g2;
+  const int tok_blocks = (M + 7) / 8;
+  const double rows = (double)M * K;
+  if (op == FP_OP_GATE) {
+    GemmParams p{};
+    p.M = M;
+    p.N = 256;
+    p.K = d;
+    p.out = t->rlog;
+    p.ldo = 256;
+    p.nseg = d / 256;
+    p.ssq_in = t->ssq;
+    p.norm_eps_in = m.rms_eps;
+    p.guard = g;
+    {
+      ProfScope ps(c, st, FP_K_ROUTER, layer, M, 2.0 * M * E * d, 0.0);
+      launch_gemm<EPI_STORE_F32>(c, t->tm_h, ly.tm_r, p, st);
+    }
+    ProfScope ps(c, st, FP_K_MOE_DISPATCH, layer, M, 0.0, rows * d * 2 * 2);
+    launch_pdl(moe_route_kernel, dim3(tok_blocks), dim3(256), 0, st, mp);
+    launch_pdl(moe_plan_kernel, dim3(1), dim3(kMoeMaxExperts), 0, st, mp);
+    launch_pdl(moe_scatter_kernel, dim3(tok_blocks), dim3(256), 0, st, mp);
+    t->moe_rows = M;
+    return FP_OK;
+  }
+  // experts
+  GemmParams p{};
+  p.M = (int)rows;
+  p.K = d;
+  p.N = 2 * I;
+  p.out = t->actp;
+  p.ldo = I;
+  p.nseg = d / 256;
+  p.ssq_in = t->ssq;
+  p.norm_eps_in = m.rms_eps;
+  p.grp_mtiles = reinterpret_cast<const int*>(t->m_mtiles);
+  p.grp_count = t->m_mtc;
+  p.grp_off = t->m_off;
+  p.grp_perm = t->m_perm;
+  p.grp_b_rows = 2 * I;
+  p.guard = g;
+  {
+    ProfScope ps(c, st, FP_K_EXPERT_GU, layer, (int)rows, 2.0 * rows * 2 * I * d, 0.0);
+    launch_gemm_grouped<EPI_SWIGLU>(c, t->tm_xperm, ly.tm_egu, p, st);
+  }
+  GemmParams q{};
+  q.M = (int)rows;
+  q.K = I;
+  q.N = d;
+  q.out = t->yperm;
+  q.ldo = d;
+  q.grp_mtiles = p.grp_mtiles;
+  q.grp_count = p.grp_count;
+  q.grp_off = p.grp_off;
+  q.grp_perm = p.grp_perm;
+  q.grp_b_rows = d;
+  q.guard = g2;
+  {
+    ProfScope ps(c, st, FP_K_EXPERT_DOWN, layer, (int)rows, 2.0 * rows * I * d, 0.0);
+    launch_gemm_grouped<EPI_STORE_BF16>(c, t->tm_actp, ly.tm_ed, q, st);
+  }
+  {
+    ProfScope ps(c, st, FP_K_MOE_COMBINE, layer, M, 0.0, (rows + 2.0 * M) * d * 2);
+    const long long units = (long long)M * (d / 256);
+    launch_pdl(moe_combine_kernel, dim3((int)((units + 7) / 8)), dim3(256), 0, st, mp);
+  }
+  if (layer == m.num_layers - 1) return launch_final(c, t, ch, layer, g2, st);
+  return FP_OK;
+}
+
 static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
   const fp_model_cfg& m = c->cfg;
   const int L = m.num_layers;
@@ -462,6 +626,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
   const bool xchg_op = c->tp_size > 1 && (op == FP_OP_O_PROJ || op == FP_OP_DOWN_PROJ);
   if (!xchg_op && !(phase & kPhasePre)) return FP_OK;  // single-phase entries run in phase 1
   const int nseg = m.hidden / 256;
+  if (m.n_experts > 0 && op >= FP_OP_GATE) return launch_moe_entry(c, t, ch, layer, op, g, g2, st);
   if (op == FP_OP_QKV_PROJ || op == FP_OP_GATE_UP_PROJ) {
     // The input RMSNorm is fused: the GEMM reads h with the norm weight folded into its weight
     // columns and scales rows by rsqrt(mean(h^2) + eps) from the segment sums in t->ssq.
@@ -573,35 +738,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
       ProfScope ps(c, st, FP_K_XCHG, layer, M, 0.0, (double)(c->tp_size + 2) * M * m.hidden * 2);
       launch_pdl(tp_allreduce_kernel, dim3(grid), dim3(256), 0, st, x);
     }
-    if (op == FP_OP_DOWN_PROJ) {
-      if (layer == L - 1 && ch.n_last > 0) {  // completion: final norm + lm_head of last tokens
-        RmsParams r{};
-        r.M = ch.n_last;
-        r.d = m.hidden;
-        r.src = t->h;
-        r.ld_src = m.hidden;
-        r.rows = t->d_last + ch.last0;
-        r.gamma = c->final_g;
-        r.out = t->xf;
-        r.ld_out = m.hidden;
-        r.eps = m.rms_eps;
-        r.guard = g2;
-        {
-          ProfScope ps(c, st, FP_K_RMS_FINAL, layer, ch.n_last, 0.0, 2.0 * ch.n_last * m.hidden * 2);
-          int rc = launch_rms(r, st);
-          if (rc) return rc;
-        }
-        GemmParams q{};
-        q.M = ch.n_last;
-        q.N = c->vocab_pad;
-        q.K = m.hidden;
-        q.out = t->logits + (long long)ch.seq0 * c->vocab_pad;
-        q.ldo = c->vocab_pad;
-        q.guard = g2;
-        ProfScope ps(c, st, FP_K_LM_HEAD, layer, ch.n_last, 2.0 * ch.n_last * q.N * q.K, 0.0);
-        launch_gemm<EPI_STORE_F32>(c, t->tm_xf, c->tm_lm, q, st);
-      }
-    }
+    if (op == FP_OP_DOWN_PROJ && layer == L - 1) return launch_final(c, t, ch, layer, g2, st);
   }
   return FP_OK;
 }
@@ -660,6 +797,15 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   REQ(cfg->n_kv_heads % tp_size == 0, "n_kv_heads must be divisible by tp_size");
   REQ(cfg->hidden % 256 == 0 && cfg->ffn % (128 * tp_size) == 0,
       "hidden%256 and ffn%(128*tp_size) required");
+  if (cfg->n_experts > 0) {
+    REQ(tp_size == 1, "MoE models run as single-GPU instances (no tensor parallelism)");
+    REQ(cfg->n_experts <= kMoeMaxExperts && cfg->top_k >= 1 && cfg->top_k <= kMoeMaxTopK &&
+            cfg->top_k <= cfg->n_experts,
+        "MoE: n_experts <= 256, 1 <= top_k <= min(16, n_experts)");
+    REQ(cfg->moe_ffn > 0 && cfg->moe_ffn % 128 == 0, "MoE: moe_ffn must be a multiple of 128");
+  } else {
+    REQ(cfg->ffn > 0, "dense models need ffn > 0");
+  }
   REQ(page_size == 128, "page_size must be 128 (one attention KV tile per page)");
   REQ(kv_pages > 0, "kv_pages must be > 0");
   CK(cudaSetDevice(device));
@@ -698,8 +844,16 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     CK(cudaMalloc(&ly.wqkv, (size_t)c->qkv_n * d * 2));
     CK(cudaMemset(ly.wqkv, 0, (size_t)c->qkv_n * d * 2));  // padding rows stay zero
     CK(cudaMalloc(&ly.wo, (size_t)d * c->qdim * 2));
-    CK(cudaMalloc(&ly.wgu, (size_t)2 * c->ffn * d * 2));
-    CK(cudaMalloc(&ly.wd, (size_t)d * c->ffn * 2));
+    if (cfg->n_experts == 0) {
+      CK(cudaMalloc(&ly.wgu, (size_t)2 * c->ffn * d * 2));
+      CK(cudaMalloc(&ly.wd, (size_t)d * c->ffn * 2));
+    } else {
+      const size_t E = cfg->n_experts, I = cfg->moe_ffn;
+      CK(cudaMalloc(&ly.wr, (size_t)256 * d * 2));
+      CK(cudaMemset(ly.wr, 0, (size_t)256 * d * 2));  // padding experts: logits 0, masked
+      CK(cudaMalloc(&ly.egu, E * 2 * I * d * 2));
+      CK(cudaMalloc(&ly.ed, E * d * I * 2));
+    }
     CK(cudaMalloc(&ly.attn_g, (size_t)d * 2));
     CK(cudaMalloc(&ly.ffn_g, (size_t)d * 2));
     {
@@ -718,8 +872,15 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     int rc;
     if ((rc = make_map(&ly.tm_qkv, ly.wqkv, c->qkv_n, d, 128))) return rc;
     if ((rc = make_map(&ly.tm_o, ly.wo, d, c->qdim, 128))) return rc;
-    if ((rc = make_map(&ly.tm_gu, ly.wgu, 2 * c->ffn, d, 128))) return rc;
-    if ((rc = make_map(&ly.tm_d, ly.wd, d, c->ffn, 128))) return rc;
+    if (cfg->n_experts == 0) {
+      if ((rc = make_map(&ly.tm_gu, ly.wgu, 2 * c->ffn, d, 128))) return rc;
+      if ((rc = make_map(&ly.tm_d, ly.wd, d, c->ffn, 128))) return rc;
+    } else {
+      const long long E = cfg->n_experts, I = cfg->moe_ffn;
+      if ((rc = make_map(&ly.tm_r, ly.wr, 256, d, 128))) return rc;
+      if ((rc = make_map(&ly.tm_egu, ly.egu, E * 2 * I, d, 128))) return rc;
+      if ((rc = make_map(&ly.tm_ed, ly.ed, E * d, I, 128))) return rc;
+    }
   }
   CK(cudaMalloc(&c->embed, (size_t)cfg->vocab * d * 2));
   c->vocab_pad = (cfg->vocab + 255) / 256 * 256;  // lm_head GEMM tiles are 256 wide
@@ -789,6 +950,9 @@ int fp_ctx_destroy(fp_ctx* c) {
     cudaFree(ly.wo);
     cudaFree(ly.wgu);
     cudaFree(ly.wd);
+    cudaFree(ly.wr);
+    cudaFree(ly.egu);
+    cudaFree(ly.ed);
     cudaFree(ly.attn_g);
     cudaFree(ly.ffn_g);
     cudaFree(ly.bqkv);
@@ -957,8 +1121,14 @@ int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, 
       __nv_bfloat16* gnew = nullptr;
       CK(cudaMalloc(&gnew, (size_t)d * 2));
       CK(cudaMemcpy(gnew, host, (size_t)d * 2, cudaMemcpyHostToDevice));
-      if (attn) fold(c, ly.wqkv, 0, 1, 0, c->qdim + 2 * c->kvdim, gnew, g);
-      else fold(c, ly.wgu, 0, 1, 0, 2 * c->ffn, gnew, g);
+      if (attn) {
+        fold(c, ly.wqkv, 0, 1, 0, c->qdim + 2 * c->kvdim, gnew, g);
+      } else if (m.n_experts > 0) {
+        fold(c, ly.wr, 0, 1, 0, m.n_experts, gnew, g);
+        fold(c, ly.egu, 0, 1, 0, 2 * m.n_experts * m.moe_ffn, gnew, g);
+      } else {
+        fold(c, ly.wgu, 0, 1, 0, 2 * c->ffn, gnew, g);
+      }
       CK(cudaMemcpyAsync(g, gnew, (size_t)d * 2, cudaMemcpyDeviceToDevice, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       cudaFree(gnew);
@@ -979,6 +1149,36 @@ int fp_weights_load(fp_ctx* c, int32_t tensor, int32_t layer, const void* host, 
       REQ(ly.q_norm != nullptr, "model has no q/k norm");
       REQ(n == 128, "q/k norm size must be head_dim");
       return load_f32_vec(tensor == FP_W_Q_NORM ? ly.q_norm : ly.k_norm, host, n);
+    case FP_W_ROUTER: {
+      REQ(ly.wr != nullptr, "model has no MoE router");
+      const long long E = m.n_experts;
+      REQ(n == E * d, "weight size mismatch");
+      CK(cudaMemcpy(ly.wr, host, (size_t)n * 2, cudaMemcpyHostToDevice));
+      fold(c, ly.wr, 0, 1, 0, (int)E, ly.ffn_g, nullptr);  // fused post-attention norm
+      CK(cudaStreamSynchronize(c->stream));
+      return FP_OK;
+    }
+    case FP_W_EXPERT_GATE:
+    case FP_W_EXPERT_UP: {
+      // per expert: [g(128) | u(128)] per 256-row block, like the dense gate/up packing
+      REQ(ly.egu != nullptr, "model has no MoE experts");
+      const long long E = m.n_experts, I = m.moe_ffn;
+      REQ(n == E * I * d, "weight size mismatch");
+      const int half = tensor == FP_W_EXPERT_UP ? 1 : 0;
+      for (long long e = 0; e < E; ++e)
+        CK(cudaMemcpy2D(ly.egu + ((size_t)e * 2 * I + half * 128) * d, (size_t)256 * d * 2,
+                        src + (size_t)e * I * d * 2, (size_t)128 * d * 2, (size_t)128 * d * 2,
+                        (size_t)(I / 128), cudaMemcpyHostToDevice));
+      fold(c, ly.egu, half * 128, (int)(E * I / 128), 256, 128, ly.ffn_g, nullptr);
+      CK(cudaStreamSynchronize(c->stream));
+      return FP_OK;
+    }
+    case FP_W_EXPERT_DOWN: {
+      REQ(ly.ed != nullptr, "model has no MoE experts");
+      REQ(n == (long long)m.n_experts * d * m.moe_ffn, "weight size mismatch");
+      CK(cudaMemcpy(ly.ed, host, (size_t)n * 2, cudaMemcpyHostToDevice));
+      return FP_OK;
+    }
   }
   return set_err(FP_ERR_ARG, "unknown tensor");
 }
@@ -1000,12 +1200,21 @@ int fp_weights_init_random(fp_ctx* c, uint64_t seed, float stdv) {
   for (auto& ly : c->layers) {
     fill(ly.wqkv, (long long)(c->qdim + 2 * c->kvdim) * d, 0.f, stdv, true);
     fill(ly.wo, d * c->qdim, 0.f, stdv, true);
-    fill(ly.wgu, 2LL * c->ffn * d, 0.f, stdv, true);
-    fill(ly.wd, d * c->ffn, 0.f, stdv, true);
     fill(ly.attn_g, d, 1.f, 0.1f);
     fill(ly.ffn_g, d, 1.f, 0.1f);
     fold(c, ly.wqkv, 0, 1, 0, c->qdim + 2 * c->kvdim, ly.attn_g, nullptr);  // fused norms
-    fold(c, ly.wgu, 0, 1, 0, 2 * c->ffn, ly.ffn_g, nullptr);
+    if (m.n_experts == 0) {
+      fill(ly.wgu, 2LL * c->ffn * d, 0.f, stdv, true);
+      fill(ly.wd, d * c->ffn, 0.f, stdv, true);
+      fold(c, ly.wgu, 0, 1, 0, 2 * c->ffn, ly.ffn_g, nullptr);
+    } else {
+      const long long E = m.n_experts, I = m.moe_ffn;
+      fill(ly.wr, E * d, 0.f, stdv);
+      fill(ly.egu, E * 2 * I * d, 0.f, stdv);
+      fill(ly.ed, E * d * I, 0.f, stdv);
+      fold(c, ly.wr, 0, 1, 0, (int)E, ly.ffn_g, nullptr);
+      fold(c, ly.egu, 0, 1, 0, (int)(E * 2 * I), ly.ffn_g, nullptr);
+    }
     if (ly.bqkv || ly.q_norm) {
       std::vector<float> v(c->qkv_n, 0.f);
       for (int i = 0; i < c->qdim + 2 * c->kvdim; ++i) v[i] = 0.02f * (float)((int)((s * 2654435761ull + i * 40503ull) % 2001) - 1000) / 1000.f;
@@ -1191,7 +1400,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   CK(cudaMallocAsync((void**)&t->ssq, M * (d / 256) * 4, up));
   CK(cudaMallocAsync((void**)&t->q, M * c->qdim * 2, up));
   CK(cudaMallocAsync((void**)&t->ao, M * c->qdim * 2, up));
-  CK(cudaMallocAsync((void**)&t->act, M * (long long)c->ffn * 2, up));
+  if (m.n_experts == 0) CK(cudaMallocAsync((void**)&t->act, M * (long long)c->ffn * 2, up));
   CK(cudaMallocAsync((void**)&t->xf, (long long)n_seqs * d * 2, up));
   CK(cudaMallocAsync((void**)&t->logits, (long long)n_seqs * c->vocab_pad * 4, up));
   CK(cudaMemsetAsync(t->logits, 0, (long long)n_seqs * c->vocab_pad * 4, up));
@@ -1202,7 +1411,42 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   int rc;
   if ((rc = make_map(&t->tm_h, t->h, M, d, 128))) return rc;
   if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
-  if ((rc = make_map(&t->tm_act, t->act, M, c->ffn, 128))) return rc;
+  if (m.n_experts == 0) {
+    if ((rc = make_map(&t->tm_act, t->act, M, c->ffn, 128))) return rc;
+  } else {
+    // MoE: router logits, routing index arrays (one allocation, zeroed: the histogram and the
+    // scatter cursors must start at 0), expert-ordered rows
+    const long long E = m.n_experts, K = m.top_k, I = m.moe_ffn, R = M * K;
+    const long long max_mt = R / 128 + E + 1;
+    CK(cudaMallocAsync((void**)&t->rlog, M * 256 * 4, up));
+    const size_t n_int = (size_t)(3 * M * K + 2 * E + (E + 1) + 1 + 2 * max_mt + R + 8);
+    CK(cudaMallocAsync((void**)&t->moe_meta, n_int * 4, up));
+    CK(cudaMemsetAsync(t->moe_meta, 0, n_int * 4, up));
+    int* q = reinterpret_cast<int*>(t->moe_meta);
+    t->m_ids = q;
+    q += M * K;
+    t->m_w = reinterpret_cast<float*>(q);
+    q += M * K;
+    t->m_slot = q;
+    q += M * K;
+    t->m_counts = q;
+    q += E;
+    t->m_cursor = q;
+    q += E;
+    t->m_off = q;
+    q += E + 1;
+    t->m_mtc = q;
+    q += 1;
+    q += (reinterpret_cast<uintptr_t>(q) & 7) ? 1 : 0;  // int2 alignment
+    t->m_mtiles = reinterpret_cast<int2*>(q);
+    q += 2 * max_mt;
+    t->m_perm = q;
+    CK(cudaMallocAsync((void**)&t->xperm, R * d * 2, up));
+    CK(cudaMallocAsync((void**)&t->actp, R * I * 2, up));
+    CK(cudaMallocAsync((void**)&t->yperm, R * d * 2, up));
+    if ((rc = make_map(&t->tm_xperm, t->xperm, R, d, 128))) return rc;
+    if ((rc = make_map(&t->tm_actp, t->actp, R, I, 128))) return rc;
+  }
   if ((rc = make_map(&t->tm_xf, t->xf, n_seqs, d, 128))) return rc;
   if ((rc = make_map(&t->tm_q, t->q, M, c->qdim, 128))) return rc;
   CK(cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming));
@@ -1258,6 +1502,11 @@ int fp_task_destroy(fp_ctx* c, fp_task* task) {
     cudaFreeAsync(t->q, st);
     cudaFreeAsync(t->ao, st);
     cudaFreeAsync(t->act, st);
+    cudaFreeAsync(t->rlog, st);
+    cudaFreeAsync(t->moe_meta, st);
+    cudaFreeAsync(t->xperm, st);
+    cudaFreeAsync(t->actp, st);
+    cudaFreeAsync(t->yperm, st);
     cudaFreeAsync(t->xf, st);
     cudaFreeAsync(t->logits, st);
     cudaFreeAsync(t->ctl, st);
@@ -1395,6 +1644,19 @@ int fp_task_logits(fp_ctx* c, fp_task* task, float* host_out) {
                        (size_t)c->cfg.vocab * 4, t->n_seqs, cudaMemcpyDeviceToHost, c->readback));
   CK(cudaStreamSynchronize(c->readback));
   return FP_OK;
+}
+
+int fp_task_read_routing(fp_ctx* c, fp_task* task, int32_t* ids, float* w, int32_t max_rows) {
+  Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && t && ids && w, "null argument");
+  REQ(c->cfg.n_experts > 0, "not a MoE model");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  const int rows = std::min(t->moe_rows, (int)max_rows);
+  const size_t n = (size_t)rows * c->cfg.top_k;
+  CK(cudaMemcpy(ids, t->m_ids, n * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(w, t->m_w, n * 4, cudaMemcpyDeviceToHost));
+  return rows;
 }
 
 int fp_task_read_kv(fp_ctx* c, fp_task* task, int32_t seq, int32_t layer, void* hk, void* hv) {

@@ -43,7 +43,8 @@ from prefillsim.engine import (  # noqa: E402
 )
 
 _BOUNDARY = _ref_engine._BOUNDARY
-_OP_NAMES = ("qkv_proj", "attn", "o_proj", "gate_up_proj", "down_proj")
+_OP_NAMES = ("qkv_proj", "attn", "o_proj", "gate_up_proj", "down_proj")  # DENSE_LAYER_OPS
+_MOE_OP_NAMES = ("qkv_proj", "attn", "o_proj", "gate", "experts")       # MOE_LAYER_OPS
 
 
 def synthetic_tokens(seed: int, vocab: int) -> Callable:
@@ -89,9 +90,10 @@ class GpuTask(ExecutionTask):
                 f"native timeline has {self.native.n_entries} entries, reference {len(timeline)}"
             )
         if binding.check_timeline:
+            names = _MOE_OP_NAMES if binding.ctx.shape.moe else _OP_NAMES
             for i, e in enumerate(timeline.entries):
                 c, l, o, _ = self.native.entry_info(i)
-                if (c, l, _OP_NAMES[o]) != (e.chunk, e.layer, e.kind.value):
+                if (c, l, names[o]) != (e.chunk, e.layer, e.kind.value):
                     raise SchedulerInvariantError(f"entry {i} mismatch: {(c, l, o)} vs {e}")
 
 
@@ -100,8 +102,10 @@ class GpuEngine(Engine):
 
     def __init__(self, params, granularity, on_arrival=None, on_completion=None, on_ack=None, *,
                  binding: GpuBinding):
-        if params.arch != "dense":
-            raise SchedulerInvariantError("GPU path implements the dense operator set only")
+        want = "moe" if binding.ctx.shape.moe else "dense"
+        if params.arch != want:
+            raise SchedulerInvariantError(
+                f"cost model arch {params.arch!r} but the GPU model is {want!r}")
         if params.num_layers != binding.ctx.shape.num_layers:
             raise SchedulerInvariantError(
                 f"cost model has {params.num_layers} layers, GPU model "

@@ -49,6 +49,10 @@ _WEIGHT_IDS = {
     "bv": _lib.W_V_BIAS,
     "q_norm": _lib.W_Q_NORM,
     "k_norm": _lib.W_K_NORM,
+    "w_router": _lib.W_ROUTER,
+    "e_gate": _lib.W_EXPERT_GATE,
+    "e_up": _lib.W_EXPERT_UP,
+    "e_down": _lib.W_EXPERT_DOWN,
 }
 
 
@@ -83,6 +87,10 @@ class PrefillContext:
             shape.rms_eps,
             int(shape.qkv_bias),
             int(shape.qk_norm),
+            int(shape.n_experts),
+            int(shape.top_k),
+            int(shape.moe_ffn),
+            int(shape.norm_topk),
         )
         h = C.c_void_p()
         _lib.check(
@@ -262,6 +270,18 @@ class PrefillTask:
         out = np.empty((len(self.lens), self.ctx.shape.vocab), np.float32)
         _lib.check(self.lib.fp_task_logits(self.ctx.h, self.h, out.ctypes.data), "fp_task_logits")
         return out
+
+    def routing(self) -> tuple[np.ndarray, np.ndarray]:
+        """MoE tap: (expert ids, weights) [rows, top_k] of the most recent gate entry."""
+        sh = self.ctx.shape
+        rows = max(self.lens) if len(self.lens) == 1 else sum(self.lens)
+        ids = np.empty((rows, sh.top_k), np.int32)
+        w = np.empty((rows, sh.top_k), np.float32)
+        n = self.lib.fp_task_read_routing(self.ctx.h, self.h, ids.ctypes.data, w.ctypes.data,
+                                          rows)
+        if n < 0:
+            _lib.check(n, "fp_task_read_routing")
+        return ids[:n], w[:n]
 
     def read_kv(self, seq: int, layer: int) -> tuple[np.ndarray, np.ndarray]:
         sh = self.ctx.shape
