@@ -632,7 +632,8 @@ def calibrated_goodput(prof, shape, args, n_instances: int = 1):
 
         base_n = config2_trace(rate=20.0 * n_instances, duration=args.goodput_duration)
         rd = dispatch.goodput_search_instances(base_n, rc, n_instances, target=0.9,
-                                               rate_bounds=(1.0, 512.0 * n_instances), tol=0.05)
+                                               rate_bounds=(1.0, 512.0 * n_instances), tol=0.05,
+                                               jobs=min(n_instances, os.cpu_count() or 1))
         out["deployment"] = {"instances": n_instances, "value": rd.value, "unit": "req/s",
                              "saturated": rd.saturated, "probes": rd.num_runs,
                              "method": "round-robin over independent instances, reference "

@@ -119,9 +119,12 @@ def run_instances(trace, n_instances: int, policy, params, seed: int = 0, runner
     clock only; results are identical to the serial run)."""
     parts = round_robin(trace, n_instances)
     if runner is None and jobs > 1 and n_instances > 1:
+        import multiprocessing as mp
         from concurrent.futures import ProcessPoolExecutor
 
-        with ProcessPoolExecutor(max_workers=min(jobs, n_instances)) as pool:
+        # spawn: the caller may hold a CUDA context and launch threads (no fork)
+        with ProcessPoolExecutor(max_workers=min(jobs, n_instances),
+                                 mp_context=mp.get_context("spawn")) as pool:
             return list(pool.map(_reference_run,
                                  [(p, policy, params, seed, record_events) for p in parts]))
     if runner is None:
