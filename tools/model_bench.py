@@ -1,8 +1,8 @@
-"""MoE prefill throughput on one B200: Qwen3-30B-A3B shape (48 layers,
+"""Prefill throughput of one model shape on one B200 (default: the MoE Qwen3-30B-A3B shape, 48 layers,
 128 experts, top-8, expert ffn 768), random bf16 weights, the bench's 16 config-2 request
 lengths as separate preemptible tasks (operator-granularity checks armed).
 
-    python tools/moe_bench.py [--steps 3] [--out gpurun_out/moe_bench.json]
+    python tools/model_bench.py [--model qwen3-30b-a3b|qwen3-8b|llama3-8b|...] [--steps 3]
 
 Reports tokens/s (CUDA events on the prefill stream) and the per-kernel-kind time and TFLOP/s
 of one profiled step; FLOPs count the router and the top_k active experts only.
@@ -74,7 +74,7 @@ def main():
         del k["flops"], k["bytes"]
     tokens = sum(LENS)
     out = {
-        "metric": "moe_prefill_tokens_per_s",
+        "metric": "prefill_tokens_per_s",
         "model": a.model,
         "value": tokens / (ms * 1e-3),
         "unit": "tok/s",
