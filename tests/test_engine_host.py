@@ -87,3 +87,27 @@ def test_preempt_resume_equals_straight(ps, gran):
     for r in trace.requests:
         solo = F.forward_logits(ctx.oshape, ctx.weights, [tok(r)], pc.chunk_tokens)[0]
         np.testing.assert_allclose(b.logits[r.id], solo, rtol=0, atol=2e-4)
+
+
+def test_moe_arch_through_gpu_engine(ps):
+    """arch='moe' (MOE_LAYER_OPS, cost_model.py:46-52): the GPU engine maps entries to gate /
+    experts, the event log equals the reference's, and stops between gate and experts resume
+    to the uninterrupted oracle logits."""
+    from paper_2602_16603_b200.engine import GpuBinding, run_on_gpu, synthetic_tokens
+
+    ctx = FakeContext("tiny-moe")
+    params = ps.CostParams(num_layers=ctx.shape.num_layers, arch="moe")
+    trace = ps.Trace((ps.Request(0, "file", 0.0, 300, 6.0), ps.Request(1, "text", 0.0004, 40, 0.25),
+                      ps.Request(2, "text", 0.0009, 70, 0.25)))
+    tok = synthetic_tokens(11, ctx.shape.vocab)
+    b = GpuBinding(ctx, tok)
+    res = run_on_gpu(trace, ps.PolicyConfig(), params, b, record_events=True)
+    ref = ps.run(trace, ps.PolicyConfig(), params, 0, record_events=True)
+    assert _events(res) == _events(ref)
+    assert res.commands["preempt"] >= 1  # the long request was preempted at least once
+    for r in trace.requests:
+        want = F.forward_logits(ctx.oshape, ctx.weights, [tok(r)])[0]
+        np.testing.assert_allclose(b.logits[r.id], want, rtol=0, atol=1e-5)
+    dense = GpuBinding(FakeContext("tiny"), tok)
+    with pytest.raises(Exception):  # a dense GPU model refuses an MoE cost model
+        run_on_gpu(trace, ps.PolicyConfig(), params, dense)
