@@ -40,10 +40,15 @@ constexpr int kTpMax = 8;
 constexpr int kTpRing = 64;
 
 // Per-rank block in peer-visible (IPC-shareable) device memory.
+constexpr int kTpFlagTiles = 8192;      // per-tile readiness flags per exchange slot
+
 struct TpShared {
   unsigned long long ready;             // exchange GEMMs whose partial sum is complete
   unsigned long long pad0[15];
   unsigned long long ring[kTpRing];     // rank 0 only: ((boundary + 1) << 2) | decision
+  // fused exchange GEMM: flags[slot][tile slot] = exchange + 1 once this rank's partial of that
+  // output tile is in part[rank][slot] (monotonic: never reset)
+  unsigned long long flags[2][kTpFlagTiles];
 };
 
 // Per-rank device-local counters (identical sequences on every rank: only entries that

@@ -55,8 +55,11 @@ struct GemmParams {
   int full_tiles;
   float* ws;
   int* tickets;     // [2][1024] per split tile slot: arrivals, done
-  int xchg;  // tensor parallel o_proj/down_proj: store the partial sum into this rank's exchange
-             // buffer (EPI_STORE_BF16) and publish it to the peers (tp_publish_partial)
+  int xchg;  // tensor parallel o_proj/down_proj (EPI_STORE_BF16): 1 = store the partial sum
+             // into this rank's exchange buffer and publish it (tp_publish_partial; a separate
+             // tp_allreduce_kernel folds the partials); 2 = FUSED: after each tile's partial
+             // store the epilogue flags the tile to the peers and folds the previous tile of
+             // every rank into the residual over NVLink, tile by tile (tp_fold_tile)
   // Fused RMSNorm. The norm weight is folded into the weight columns (W' = W diag(gamma)), so
   // rmsnorm(h) W^T = rsqrt(mean(h^2) + eps) * (h W'^T): the GEMM reads the residual stream h
   // directly and the EPI_QKV / EPI_SWIGLU epilogue scales its row by the rsqrt factor, built
@@ -202,6 +205,68 @@ DEVI void store16_bf16(__nv_bfloat16* dst, const float* v) {
     u.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
     st_global_v4(dst + 8 * i, u);
   }
+}
+
+// Fused tensor-parallel exchange (GemmParams::xchg == 2), run by the 4 epilogue warps (one
+// tile row each): wait until every rank has flagged its partial of this output tile, then
+// h[m, n0:n0+256] = bf16(h + part_0 + part_1 + ...) (fp32, rank order: the same bits as
+// tp_allreduce_kernel on every rank) and the next fused norm's segment sum of squares.
+DEVI void tp_fold_tile(const GemmParams& p, const TpDev* tp, int slot, unsigned long long want,
+                       int fidx, int m_base, int row_end, int n0, int nb) {
+  const int row = threadIdx.x - 128;  // epilogue threads 128..255
+  if (row == 0) {
+    for (int r = 0; r < tp->size; ++r)
+      while (ld_acquire_sys_u64(&tp->peer[r]->flags[slot][fidx]) < want) __nanosleep(64);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int m = m_base + row;
+  if (m >= row_end) return;
+  __nv_bfloat16* hrow = p.resid + (long long)m * p.ldr + n0;
+  float ss = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < 8; ++c) {  // 32 columns at a time, every rank's loads in flight
+    uint4 v[kTpMax][4];
+#pragma unroll
+    for (int r = 0; r < kTpMax; ++r)
+      if (r < tp->size) {
+        const __nv_bfloat16* src = tp->part[r][slot] + (long long)m * p.ldo + n0 + c * 32;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[r][i] = ld_cg_v4(src + 8 * i);
+      }
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 h = ld_global_v4(hrow + c * 32 + 8 * i);
+      const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(hw[j]);
+        acc[8 * i + 2 * j] = f.x;
+        acc[8 * i + 2 * j + 1] = f.y;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kTpMax; ++r)
+      if (r < tp->size) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t w4[4] = {v[r][i].x, v[r][i].y, v[r][i].z, v[r][i].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack_bf16x2(w4[j]);
+            acc[8 * i + 2 * j] += f.x;
+            acc[8 * i + 2 * j + 1] += f.y;
+          }
+        }
+      }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {  // the next norm sees the bf16-rounded values
+      const float rv = __bfloat162float(__float2bfloat16(acc[i]));
+      ss += rv * rv;
+    }
+    store_row32_bf16(hrow + c * 32, acc);
+  }
+  if (p.ssq_out) p.ssq_out[(long long)m * p.nseg + nb] = ss;
 }
 
 // Epilogue item g (0..7) of tile row r (token row m) of a split tile; n0 / nb = the tile's first
@@ -539,6 +604,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
     }
   } else if (warp >= 4) {
+    // fused TP exchange state (xchg == 2): the previous tile still to be folded
+    int prev_fidx = -1, prev_m = 0, prev_end = 0, prev_n0 = 0, prev_nb = 0;
+    const int xc_now = (EPI == EPI_STORE_BF16 && p.xchg) ? p.guard.tp->local->xcount : 0;
+    const int xslot = xc_now & 1;
+    const unsigned long long xwant = (unsigned long long)xc_now + 1;
     const int q = warp & 3;  // TMEM lane quadrant
     const int row = q * 32 + lane;
     int it = 0;
@@ -808,6 +878,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if (threadIdx.x == 128) GEMM_STAMP(7);
       release_acc(acc);
+      if constexpr (EPI == EPI_STORE_BF16 && MODE == 0) {
+        if (p.xchg == 2) {
+          // flag this tile's partial to the peers, then fold the previous tile of all ranks
+          // (its peers' partials are due by now) while the tensor core runs the next tile
+          const TpDev* tp = p.guard.tp;
+          __threadfence_system();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const int fidx = tile * CG + (int)rank;
+          if (row == 0)
+            st_release_sys_u64(&tp->peer[tp->rank]->flags[xslot][fidx], xwant);
+          if (prev_fidx >= 0)
+            tp_fold_tile(p, tp, xslot, xwant, prev_fidx, prev_m, prev_end, prev_n0, prev_nb);
+          prev_fidx = fidx;
+          prev_m = row_a;
+          prev_end = row_end;
+          prev_n0 = n0;
+          prev_nb = nb;
+        }
+      }
+    }
+    if constexpr (EPI == EPI_STORE_BF16 && MODE == 0) {
+      if (p.xchg == 2 && prev_fidx >= 0)
+        tp_fold_tile(p, p.guard.tp, xslot, xwant, prev_fidx, prev_m, prev_end, prev_n0, prev_nb);
     }
     if (EPI == EPI_STORE_BF16 && p.xchg) __threadfence_system();  // partials visible to peers
   }
@@ -816,7 +909,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/arrivals are all done
   else __syncthreads();
-  if (EPI == EPI_STORE_BF16 && p.xchg && run && threadIdx.x == 0) tp_publish_partial(p.guard.tp);
+  if (EPI == EPI_STORE_BF16 && p.xchg == 1 && run && threadIdx.x == 0) tp_publish_partial(p.guard.tp);
+  if (EPI == EPI_STORE_BF16 && p.xchg == 2 && run && threadIdx.x == 0) {
+    // the last CTA out completes the exchange (every tile of every rank is folded)
+    const TpDev* tp = p.guard.tp;
+    __threadfence();
+    if (atomicAdd(&tp->local->ar_ctr, 1) == (int)(gridDim.x * gridDim.y * gridDim.z) - 1) {
+      tp->local->ar_ctr = 0;
+      tp->local->xcount = tp->local->xcount + 1;
+      __threadfence();
+    }
+  }
   if (threadIdx.x == 64) GEMM_STAMP(11);
   if (warp == 2) {
     tc_fence_after();

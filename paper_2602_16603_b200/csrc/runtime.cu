@@ -185,6 +185,7 @@ struct fp_ctx {
   std::vector<void*> tp_opened;  // peer blocks opened through IPC
   bool tp_connected = false;
   bool tp_lockstep = false;
+  bool tp_fused = true;  // FP_TP_FUSED=0: GEMM + tp_allreduce_kernel even with one process per GPU
   std::vector<Layer> layers;
   __nv_bfloat16 *embed = nullptr, *final_g = nullptr, *lm_head = nullptr;
   CUtensorMap tm_lm;
@@ -348,7 +349,11 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   if (c->ws && EPI != EPI_STORE_F32)
     choose_splits(tiles, p.K / kGemmBK, slots, &p.full_tiles, &p.splits, split_tail_ok(EPI, p.K),
                   split_overhead(EPI));
-  if (c->force_splits > 0) {  // experiments only (FP_FORCE_SPLITS)
+  if (p.xchg) {  // TP exchange GEMMs publish / fold their partials per tile: never split
+    p.splits = 1;
+    p.full_tiles = tiles;
+  }
+  if (c->force_splits > 0 && !p.xchg) {  // experiments only (FP_FORCE_SPLITS)
     const int rem = tiles % slots;
     p.splits = rem ? c->force_splits : 1;
     p.full_tiles = tiles - rem;
@@ -719,13 +724,23 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
       ProfScope ps(c, st, kind, layer, M, 2.0 * M * p.N * p.K, 0.0);
       launch_gemm<EPI_RESID>(c, ta, tb, p, st);
     } else {
+      // One process per GPU: the exchange is FUSED into the GEMM (each tile's partial is
+      // flagged to the peers and folded tile by tile over NVLink inside the same kernel).
+      // Ranks in lock step on one device (launched one after another) cannot wait on each
+      // other inside a kernel: they use the GEMM + tp_allreduce_kernel pair.
+      const bool fused = !c->tp_lockstep && c->tp_fused &&
+                         (long long)((M + 127) / 128) * (m.hidden / 256) <= kTpFlagTiles;
       if (phase & kPhasePre) {
-        p.xchg = 1;
+        p.xchg = fused ? 2 : 1;
         p.ldo = m.hidden;
         ProfScope ps(c, st, kind, layer, M, 2.0 * M * p.N * p.K, 0.0);
         launch_gemm<EPI_STORE_BF16>(c, ta, tb, p, st);
       }
-      if (!(phase & kPhasePost)) return FP_OK;
+      if (fused || !(phase & kPhasePost)) {
+        if (fused && op == FP_OP_DOWN_PROJ && layer == L - 1)
+          return launch_final(c, t, ch, layer, g2, st);
+        return FP_OK;
+      }
       XchgParams x{};
       x.M = M;
       x.d = m.hidden;
@@ -911,6 +926,7 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     if (const char* e = getenv("FP_PAIR_GEMM")) c->use_pair_gemm = atoi(e) != 0;
     if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
+    if (const char* e = getenv("FP_TP_FUSED")) c->tp_fused = atoi(e) != 0;
     if (const char* e = getenv("FP_GEMM_STAMPS"))
       if (atoi(e)) CK(cudaMalloc(&c->gemm_dbg, (size_t)4096 * 16 * sizeof(unsigned long long)));
     const uint64_t rows = (uint64_t)L * kv_pages * 2 * c->hkv * page_size;

@@ -3,8 +3,11 @@ exchange their exchange-block handles over a gloo group (connect_tp_dist), map e
 blocks through CUDA IPC and run independently -- no lock step, each rank's launch stream is its
 own. On the single-GPU test box both processes share the device (time-sliced contexts), which
 exercises the same cross-process waits (exchange readiness, rank-0 decision ring) the 8-GPU box
-runs over NVLink. Checks: logits vs the fp32 oracle, identical logits on both ranks, and a
-preemption signalled on rank 0 stops both ranks at the same entry."""
+runs over NVLink. Checks: logits vs the fp32 oracle, identical logits on both ranks, a
+preemption signalled on rank 0 stops both ranks at the same entry, and the FUSED exchange (the
+o_proj / down_proj GEMM flags each tile's partial and folds every rank's tile over peer memory
+inside the same kernel) matches the GEMM + tp_allreduce_kernel pair (same rank-order sums; only
+the summation order of the next norm's sum of squares differs, so within 1%)."""
 
 import os
 import random
@@ -20,10 +23,11 @@ pytestmark = pytest.mark.gpu
 NAME = "tiny-qwen2-tp"
 
 
-def _rank_main(rank, size, port, q):
+def _rank_main(rank, size, port, q, fused=True):
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                      FP_TP_FUSED="1" if fused else "0")
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
         from paper_2602_16603_b200.config import SHAPES
@@ -71,12 +75,11 @@ def _rank_main(rank, size, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.timeout(300)
-def test_tp2_two_processes_ipc():
+def _run_group(fused):
     size, port = 2, random.randint(20000, 40000)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank_main, args=(r, size, port, q)) for r in range(size)]
+    procs = [ctx.Process(target=_rank_main, args=(r, size, port, q, fused)) for r in range(size)]
     for p in procs:
         p.start()
     try:
@@ -89,6 +92,12 @@ def test_tp2_two_processes_ipc():
             p.join(60)
             if p.is_alive():
                 p.kill()
+    return res
+
+
+@pytest.mark.timeout(300)
+def test_tp2_two_processes_ipc():
+    res = _run_group(fused=True)
     shape = F.SHAPES[NAME]
     w = F.make_weights(shape, 4321)
     ref = F.forward_logits(shape, w, F.make_tokens([300, 37], shape.vocab, 11))
@@ -102,3 +111,15 @@ def test_tp2_two_processes_ipc():
     assert np.array_equal(res[0][3], s0) and np.array_equal(res[1][3], s0)
     c0, c1 = res[0][4], res[1][4]
     assert (c0["exchanges"], c0["boundaries"]) == (c1["exchanges"], c1["boundaries"])
+
+
+
+@pytest.mark.timeout(300)
+def test_tp2_fused_exchange_matches_two_kernel_exchange():
+    fused, split = _run_group(fused=True), _run_group(fused=False)
+    for r in range(2):
+        for i in (0, 3):  # straight, preempted + resumed
+            a, b = fused[r][i], split[r][i]
+            assert np.abs(a - b).max() / np.abs(b).max() <= 0.01
+        assert np.array_equal(fused[r][0], fused[r][3])  # fused: preemption changes no bits
+        assert fused[r][4]["exchanges"] == split[r][4]["exchanges"]
