@@ -241,8 +241,9 @@ int fp_op_gemm(fp_ctx* ctx, int32_t epi, const void* A, const void* B, void* C, 
 int fp_op_rmsnorm(fp_ctx* ctx, const void* x, const void* gamma, void* out, int32_t M,
                   int32_t d, float eps);
 /* GEMM tiling override for experiments and split-K parity tests: pair = -1 auto, 0 single-CTA
- * tiles, 1 CTA-pair tiles; splits = 0 auto, S >= 1 forces S K-slices on the partial-wave tiles
- * (clamped so the split units fit one round of the persistent grid). */
+ * tiles, 1 CTA-pair tiles, 2 narrow 128 x 128 tiles (residual / QKV epilogues); splits = 0
+ * auto, S >= 1 forces S K-slices on the partial-wave tiles (clamped so the split units fit one
+ * round of the persistent grid). */
 int fp_ctx_set_gemm_policy(fp_ctx* ctx, int32_t pair, int32_t splits);
 /* Diagnostics: with FP_GEMM_STAMPS=1 in the environment at fp_ctx_create, every fp_op_gemm
  * launch records per-CTA phase stamps (%globaltimer ns, 16 slots per CTA: entry, prologue done,

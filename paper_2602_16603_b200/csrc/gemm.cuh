@@ -63,7 +63,7 @@ struct GemmParams {
   // Fused RMSNorm. The norm weight is folded into the weight columns (W' = W diag(gamma)), so
   // rmsnorm(h) W^T = rsqrt(mean(h^2) + eps) * (h W'^T): the GEMM reads the residual stream h
   // directly and the EPI_QKV / EPI_SWIGLU epilogue scales its row by the rsqrt factor, built
-  // from `ssq_in` = per-row sums of squares of h in 256-column segments [M, nseg] (summed in
+  // from `ssq_in` = per-row sums of squares of h in 128-column segments [M, nseg] (summed in
   // segment order: deterministic). EPI_RESID writes those segment sums of the new h into
   // `ssq_out` (tile n-block nb = segment nb) for the next norm.
   int nseg;
@@ -207,6 +207,26 @@ DEVI void store16_bf16(__nv_bfloat16* dst, const float* v) {
   }
 }
 
+// rsqrt(mean(h^2) + eps) of a row from its 128-column segment sums of squares (nseg is a
+// multiple of 4: hidden % 512 == 0), summed in segment order with all loads in flight.
+DEVI float fused_norm_rsqrt(const float* sp, int nseg, float eps) {
+  const float4* s4 = reinterpret_cast<const float4*>(sp);
+  float ssum = 0.f;
+  int i = 0;
+  for (; i + 4 <= nseg / 4; i += 4) {
+    float4 a[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[j] = __ldg(s4 + i + j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ssum = (((ssum + a[j].x) + a[j].y) + a[j].z) + a[j].w;
+  }
+  for (; i < nseg / 4; ++i) {
+    const float4 a = __ldg(s4 + i);
+    ssum = (((ssum + a.x) + a.y) + a.z) + a.w;
+  }
+  return rsqrtf(ssum / (float)(nseg * 128) + eps);
+}
+
 // Fused tensor-parallel exchange (GemmParams::xchg == 2), run by the 4 epilogue warps (one
 // tile row each): wait until every rank has flagged its partial of this output tile, then
 // h[m, n0:n0+256] = bf16(h + part_0 + part_1 + ...) (fp32, rank order: the same bits as
@@ -265,8 +285,11 @@ DEVI void tp_fold_tile(const GemmParams& p, const TpDev* tp, int slot, unsigned 
       ss += rv * rv;
     }
     store_row32_bf16(hrow + c * 32, acc);
+    if (c == 3 || c == 7) {  // 128-column segment complete
+      if (p.ssq_out) p.ssq_out[(long long)m * p.nseg + nb * 2 + (c >> 2)] = ss;
+      ss = 0.f;
+    }
   }
-  if (p.ssq_out) p.ssq_out[(long long)m * p.nseg + nb] = ss;
 }
 
 // Epilogue item g (0..7) of tile row r (token row m) of a split tile; n0 / nb = the tile's first
@@ -287,10 +310,7 @@ __device__ __noinline__ void split_item_epilogue(const GemmParams& p, const Gmem
   float rs = 1.f;  // fused input RMSNorm factor of the row
   if ((EPI == EPI_QKV || EPI == EPI_SWIGLU || EPI == EPI_STORE_F32) && p.ssq_in != nullptr &&
       valid) {
-    const float* sp = p.ssq_in + (long long)m * p.nseg;
-    float ssum = 0.f;
-    for (int i = 0; i < p.nseg; ++i) ssum += __ldg(sp + i);
-    rs = rsqrtf(ssum / (float)(p.nseg * 256) + p.norm_eps_in);
+    rs = fused_norm_rsqrt(p.ssq_in + (long long)m * p.nseg, p.nseg, p.norm_eps_in);
   }
   float v[32];
   if constexpr (EPI == EPI_RESID) {
@@ -318,10 +338,11 @@ __device__ __noinline__ void split_item_epilogue(const GemmParams& p, const Gmem
       }
       store_row32_bf16(hrow, v);
     }
-    float tot = 0.f;
+    float tot = 0.f;  // chunks 0-3 and 4-7: the two 128-column segments of the tile
 #pragma unroll
-    for (int j = 0; j < 8; ++j) tot += __shfl_sync(0xffffffffu, ss, (lane & ~7) + j);
-    if (valid && g == 0 && p.ssq_out != nullptr) p.ssq_out[(long long)m * p.nseg + nb] = tot;
+    for (int j = 0; j < 4; ++j) tot += __shfl_sync(0xffffffffu, ss, (lane & ~3) + j);
+    if (valid && (g & 3) == 0 && p.ssq_out != nullptr)
+      p.ssq_out[(long long)m * p.nseg + nb * 2 + (g >> 2)] = tot;
   } else if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32) {
     if (!valid) return;
     sum.get(r, g * 32, g * 32 + 16, v);
@@ -691,10 +712,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if ((EPI == EPI_QKV || EPI == EPI_SWIGLU || EPI == EPI_STORE_F32) && p.ssq_in != nullptr &&
           live) {
         const int tok = MODE == 2 ? p.grp_perm[m] : m;
-        const float* sp = p.ssq_in + (long long)tok * p.nseg;
-        float ssum = 0.f;
-        for (int i = 0; i < p.nseg; ++i) ssum += __ldg(sp + i);
-        rs = rsqrtf(ssum / (float)(p.nseg * 256) + p.norm_eps_in);
+        rs = fused_norm_rsqrt(p.ssq_in + (long long)tok * p.nseg, p.nseg, p.norm_eps_in);
       }
       auto load32 = [&](int col, float* v) {
         uint32_t r[32];
@@ -739,8 +757,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             store_row32_bf16(hrow + c * 32, v);
           }
+          if ((c & 3) == 3) {  // a 128-column segment of the new h is complete
+            if (live && p.ssq_out) p.ssq_out[(long long)m * p.nseg + nb * (BN / 128) + (c >> 2)] = ss;
+            ss = 0.f;
+          }
         }
-        if (live && p.ssq_out) p.ssq_out[(long long)m * p.nseg + nb] = ss;
       } else if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32) {
         void* out = p.out;
         if (EPI == EPI_STORE_BF16 && p.xchg) {

@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const MoeParams p) {
   }
   st_global_v4(p.h_out + (long long)t * p.d + c, make_uint4(o4[0], o4[1], o4[2], o4[3]));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0 && p.ssq) p.ssq[(long long)t * nseg + sg] = ss;
+  for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);  // half warps
+  if ((lane & 15) == 0 && p.ssq) p.ssq[(long long)t * nseg * 2 + sg * 2 + (lane >> 4)] = ss;
 }
 
 }  // namespace fp

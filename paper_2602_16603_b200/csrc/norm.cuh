@@ -21,8 +21,8 @@ struct RmsParams {
   __nv_bfloat16* out;  // [M, ld_out]; null: only the embedding copy + segment sums
   long long ld_out;
   float eps;
-  int nseg;            // with ssq: d / 256
-  float* ssq;          // optional [M, nseg]: sums of squares per 256-column segment (the
+  int nseg;            // with ssq: d / 128
+  float* ssq;          // optional [M, nseg]: sums of squares per 128-column segment (the
                        // fused-norm input of the next GEMM, see GemmParams::ssq_in)
   Guard guard;
 };
@@ -51,9 +51,11 @@ __global__ void __launch_bounds__(1024) rmsnorm_kernel(const RmsParams p) {
     ss += v.x * v.x + v.y * v.y;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (lane == 0) red[warp] = ss;  // one warp = one 256-column segment
-  if (p.ssq && lane == 0) p.ssq[(long long)row * p.nseg + warp] = ss;
+  for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  // a half warp = one 128-column segment
+  if (p.ssq && (lane & 15) == 0) p.ssq[(long long)row * p.nseg + warp * 2 + (lane >> 4)] = ss;
+  ss += __shfl_xor_sync(0xffffffffu, ss, 16);
+  if (lane == 0) red[warp] = ss;
   if (p.ids && p.h_out) st_global_v4(p.h_out + (long long)row * p.ld_h + c, raw);
   if (p.out == nullptr) return;
   __syncthreads();

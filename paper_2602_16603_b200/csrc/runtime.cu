@@ -148,7 +148,7 @@ struct Task {
   int *d_ids, *d_pos, *d_tpage, *d_bt, *d_last;
   AttnTile* d_items;
   __nv_bfloat16 *h, *q, *ao, *act, *xf;
-  float* ssq;  // [max_m, hidden/256] segment sums of squares of h (fused RMSNorm input)
+  float* ssq;  // [max_m, hidden/128] segment sums of squares of h (fused RMSNorm input)
   float* logits;
   TaskCtl* ctl;
   CUtensorMap tm_h, tm_ao, tm_act, tm_xf, tm_q;
@@ -298,8 +298,8 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // L2, the inter-CTA barrier and the reduction (~8 us measured on B200, tools/split_sweep.py and
 // tools/gemm_stamps.py). A split must win by > 15%. tail_ok = false restricts splitting to
 // launches whose tiles all split (no full wave in front).
-static constexpr double kSplitOverheadKb = 24.0;
-static constexpr double kSplitOverheadKbQkv = 40.0;  // RoPE / KV-scatter items cost more
+static constexpr double kSplitOverheadKb = 44.0;
+static constexpr double kSplitOverheadKbQkv = 60.0;  // RoPE / KV-scatter items cost more
 // Tails behind full waves split only for long K (down_proj): the split-capable instantiation
 // runs the full-wave tiles with more register pressure (measured slower for QKV / SwiGLU).
 static bool split_tail_ok(int epi, int K) {
@@ -329,31 +329,31 @@ static double choose_splits(int tiles, int num_k, int num_sms, int* full_tiles, 
   return full_cost + best_t;
 }
 
-template <int EPI, int CG>
+template <int EPI, int CG, int BN = 256>
 static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b, GemmParams p,
                            cudaStream_t st) {
-  constexpr int BN = 256;
   using Cfg = GemmCfg<BN, CG>;
   static bool attr = false;
   if (!attr) {
-    for (auto k : {gemm_bf16_tn_kernel<BN, EPI, CG, 0>, gemm_bf16_tn_kernel<BN, EPI, CG, 1>}) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-      if (CG == 2) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    }
+    cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI, CG, 0>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if constexpr (BN == 256)
+      cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI, CG, 1>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     attr = true;
   }
   const int tiles = ((p.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * (p.N / BN);
   const int slots = c->num_sms / CG;  // concurrent tiles (CTA pairs)
   p.splits = 1;
   p.full_tiles = tiles;
-  if (c->ws && EPI != EPI_STORE_F32)
+  if (c->ws && EPI != EPI_STORE_F32 && BN == 256)
     choose_splits(tiles, p.K / kGemmBK, slots, &p.full_tiles, &p.splits, split_tail_ok(EPI, p.K),
                   split_overhead(EPI));
   if (p.xchg) {  // TP exchange GEMMs publish / fold their partials per tile: never split
     p.splits = 1;
     p.full_tiles = tiles;
   }
-  if (c->force_splits > 0 && !p.xchg) {  // experiments only (FP_FORCE_SPLITS)
+  if (c->force_splits > 0 && !p.xchg && BN == 256) {  // experiments only (FP_FORCE_SPLITS)
     const int rem = tiles % slots;
     p.splits = rem ? c->force_splits : 1;
     p.full_tiles = tiles - rem;
@@ -384,8 +384,13 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
-  if (p.splits > 1) cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 1>, a, b, p);
-  else cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 0>, a, b, p);
+  if constexpr (BN == 256) {
+    if (p.splits > 1) {
+      cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 1>, a, b, p);
+      return;
+    }
+  }
+  cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 0>, a, b, p);
 }
 
 // Grouped (MoE expert) GEMM: persistent over the device-side m-tile table (gemm.cuh MODE 2).
@@ -421,9 +426,39 @@ static bool pick_pair(const fp_ctx* c, int epi, int M, int N, int K) {
   return t2 < t1;
 }
 
+// Narrow tiles (128 x 128, one CTA, unsplit) for under-filled residual / QKV GEMMs: twice the
+// tiles of the 256-wide kernel at the same M, so mid-size requests fill the machine without
+// split-K. Cost in k-block units of a 128 x 256 tile: kNarrowKbCost per k-block (a narrow
+// k-block is half the MMA work but moves 2/3 of the shared-memory bytes) + 4 of pipeline fill;
+// chosen when it beats the best 256-wide plan by 10%.
+static constexpr double kNarrowKbCost = 0.8;
+static bool pick_narrow(const fp_ctx* c, int epi, int M, int N, int K) {
+  if (epi != EPI_RESID && epi != EPI_QKV) return false;
+  if (c->force_pair == 2) return true;
+  if (c->force_pair >= 0 || c->force_splits > 0) return false;
+  const int num_k = K / kGemmBK, nN = N / 256;
+  int ft, sp;
+  const bool tail = split_tail_ok(epi, K);
+  const double ov = split_overhead(epi);
+  double t256 = choose_splits(((M + 127) / 128) * nN, num_k, c->num_sms, &ft, &sp, tail, ov);
+  if (c->use_pair_gemm && M > kGemmBM)
+    t256 = std::min(t256, choose_splits(((M + 255) / 256) * nN, num_k, c->num_sms / 2, &ft, &sp,
+                                        tail, ov) / 1.09);
+  const long long tiles = (long long)((M + 127) / 128) * (N / 128);
+  const double waves = std::ceil((double)tiles / c->num_sms);
+  const double t128 = waves * (kNarrowKbCost * num_k + 4.0);
+  return t128 * 1.1 < t256;
+}
+
 template <int EPI>
 static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
                         const GemmParams& p, cudaStream_t st) {
+  if constexpr (EPI == EPI_RESID || EPI == EPI_QKV) {
+    if (!p.xchg && pick_narrow(c, EPI, p.M, p.N, p.K)) {
+      launch_gemm_cg<EPI, 1, 128>(c, a, b, p, st);
+      return;
+    }
+  }
   if (pick_pair(c, EPI, p.M, p.N, p.K)) launch_gemm_cg<EPI, 2>(c, a, b, p, st);
   else launch_gemm_cg<EPI, 1>(c, a, b, p, st);
 }
@@ -540,7 +575,7 @@ static int launch_moe_entry(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, 
     p.K = d;
     p.out = t->rlog;
     p.ldo = 256;
-    p.nseg = d / 256;
+    p.nseg = d / 128;
     p.ssq_in = t->ssq;
     p.norm_eps_in = m.rms_eps;
     p.guard = g;
@@ -562,7 +597,7 @@ static int launch_moe_entry(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, 
   p.N = 2 * I;
   p.out = t->actp;
   p.ldo = I;
-  p.nseg = d / 256;
+  p.nseg = d / 128;
   p.ssq_in = t->ssq;
   p.norm_eps_in = m.rms_eps;
   p.grp_mtiles = reinterpret_cast<const int*>(t->m_mtiles);
@@ -630,7 +665,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
 
   const bool xchg_op = c->tp_size > 1 && (op == FP_OP_O_PROJ || op == FP_OP_DOWN_PROJ);
   if (!xchg_op && !(phase & kPhasePre)) return FP_OK;  // single-phase entries run in phase 1
-  const int nseg = m.hidden / 256;
+  const int nseg = m.hidden / 128;  // fused-norm sum-of-squares segments
   if (m.n_experts > 0 && op >= FP_OP_GATE) return launch_moe_entry(c, t, ch, layer, op, g, g2, st);
   if (op == FP_OP_QKV_PROJ || op == FP_OP_GATE_UP_PROJ) {
     // The input RMSNorm is fused: the GEMM reads h with the norm weight folded into its weight
@@ -810,8 +845,8 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   REQ(cfg->head_dim == 128, "head_dim must be 128");
   REQ(cfg->n_heads % cfg->n_kv_heads == 0, "n_heads must be a multiple of n_kv_heads");
   REQ(cfg->n_kv_heads % tp_size == 0, "n_kv_heads must be divisible by tp_size");
-  REQ(cfg->hidden % 256 == 0 && cfg->ffn % (128 * tp_size) == 0,
-      "hidden%256 and ffn%(128*tp_size) required");
+  REQ(cfg->hidden % 512 == 0 && cfg->ffn % (128 * tp_size) == 0,
+      "hidden%512 and ffn%(128*tp_size) required");
   if (cfg->n_experts > 0) {
     REQ(tp_size == 1, "MoE models run as single-GPU instances (no tensor parallelism)");
     REQ(cfg->n_experts <= kMoeMaxExperts && cfg->top_k >= 1 && cfg->top_k <= kMoeMaxTopK &&
@@ -1023,7 +1058,7 @@ int fp_debug_gemm_stamps(fp_ctx* c, uint64_t* out, int32_t max_ctas) {
   return FP_OK;
 }
 int fp_ctx_set_gemm_policy(fp_ctx* c, int32_t pair, int32_t splits) {
-  REQ(c && pair >= -1 && pair <= 1 && splits >= 0 && splits <= 32, "bad gemm policy");
+  REQ(c && pair >= -1 && pair <= 2 && splits >= 0 && splits <= 32, "bad gemm policy");
   c->force_pair = pair;
   c->force_splits = splits;
   return FP_OK;
@@ -1413,7 +1448,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   // workspaces (resume state lives here: h + the live intermediate)
   const long long M = t->max_m, d = m.hidden;
   CK(cudaMallocAsync((void**)&t->h, M * d * 2, up));
-  CK(cudaMallocAsync((void**)&t->ssq, M * (d / 256) * 4, up));
+  CK(cudaMallocAsync((void**)&t->ssq, M * (d / 128) * 4, up));
   CK(cudaMallocAsync((void**)&t->q, M * c->qdim * 2, up));
   CK(cudaMallocAsync((void**)&t->ao, M * c->qdim * 2, up));
   if (m.n_experts == 0) CK(cudaMallocAsync((void**)&t->act, M * (long long)c->ffn * 2, up));

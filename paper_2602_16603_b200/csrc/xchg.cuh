@@ -94,8 +94,8 @@ __global__ void __launch_bounds__(256) tp_allreduce_kernel(const XchgParams p) {
         ss += f.x * f.x + f.y * f.y;
       }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-      if (lane == 0) p.ssq[m * nseg + sg] = ss;
+      for (int off = 8; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      if ((lane & 15) == 0) p.ssq[m * nseg * 2 + sg * 2 + (lane >> 4)] = ss;  // 128-col segments
     }
   }
   // the last CTA advances the exchange counter (read by the next exchange GEMM / all-reduce)

@@ -165,3 +165,25 @@ def test_qwen_variants_vs_hf_and_oracle(golden_dir, name):
         assert rel_err(v, ot.v_cache[r][1]) <= KV_ATOL_FRAC
     t.destroy()
     ctx.close()
+
+
+@pytest.mark.parametrize("policy", [2, 0])
+def test_forced_gemm_tiling_vs_oracle(tiny, policy):
+    """Every GEMM of the forward with narrow 128 x 128 tiles (policy 2: residual and QKV
+    epilogues) or single-CTA 256-wide tiles (policy 0): logits and KV within tolerance."""
+    shape, w, ctx = tiny
+    tokens = F.make_tokens([37, 300, 130], shape.vocab, 21)
+    ot = F.OracleTask(shape, w, tokens, None)
+    ot.run_all()
+    try:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, policy, 0)
+        t = run_straight(ctx, tokens)
+        lg = t.logits()
+        kv = [t.read_kv(r, shape.num_layers - 1) for r in range(3)]
+        t.destroy()
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+    assert rel_err(lg, ot.logits) <= LOGIT_ATOL_FRAC
+    for r, (k, v) in enumerate(kv):
+        assert rel_err(k, ot.k_cache[r][shape.num_layers - 1]) <= KV_ATOL_FRAC
+        assert rel_err(v, ot.v_cache[r][shape.num_layers - 1]) <= KV_ATOL_FRAC

@@ -99,3 +99,27 @@ def test_gemm_forced_split(ctx, M, N, K, pair, splits, epi):
     scale = ref.abs().max().item()
     tol = 1e-5 * scale * K ** 0.5 if epi == 1 else 2 ** -7 * scale + 1e-3
     assert err <= tol, (err, scale)
+
+
+@pytest.mark.parametrize("M,N,K", [(42, 4096, 4096), (450, 4096, 4096), (1000, 1024, 14336),
+                                   (1, 256, 128)])
+def test_gemm_narrow_tiles(ctx, M, N, K):
+    """128 x 128 tiles (residual epilogue), forced: within bf16 tolerance of fp32."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    out = torch.randn(M, N, device="cuda", dtype=torch.bfloat16, generator=g)
+    ref = A.float() @ B.float().t() + out.float()
+    try:
+        _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, 2, 0))
+        torch.cuda.synchronize()
+        _lib.check(ctx.lib.fp_op_gemm(ctx.h, 2, A.data_ptr(), B.data_ptr(), out.data_ptr(), M, N, K))
+        ctx.sync()
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2 ** -7 * ref.abs().max().item() + 1e-3, err

@@ -34,7 +34,7 @@ def main():
         for M in MS:
             A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
             C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-            for pair, S in [(-1, 0)] + [(pair, S) for pair in (0, 1) for S in SPLITS]:
+            for pair, S in [(-1, 0), (2, 0)] + [(pair, S) for pair in (0, 1) for S in SPLITS]:
                 if True:
                     lib.fp_ctx_set_gemm_policy(ctx.h, pair, S)
                     i = [0]
