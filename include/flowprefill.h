@@ -240,6 +240,14 @@ int fp_op_gemm(fp_ctx* ctx, int32_t epi, const void* A, const void* B, void* C, 
                int32_t N, int32_t K);
 int fp_op_rmsnorm(fp_ctx* ctx, const void* x, const void* gamma, void* out, int32_t M,
                   int32_t d, float eps);
+/* out[M, F] = silu(x W_gate^T) * (x W_up^T): the gate_up_proj GEMM with its SwiGLU epilogue. */
+int fp_op_gate_up_swiglu(fp_ctx* ctx, const void* x, const void* w_gate, const void* w_up,
+                         void* out, int32_t M, int32_t F, int32_t K);
+/* Causal prefill attention of one request's last n_q tokens over kv_len keys (prefix =
+ * kv_len - n_q): q/out [n_q, n_heads*128], k/v [kv_len, n_kv_heads*128] (bf16, device); K/V go
+ * through the paged pool like the forward pass (borrowed free pages). */
+int fp_op_attn_prefill(fp_ctx* ctx, const void* q, const void* k, const void* v, void* out,
+                       int32_t n_q, int32_t kv_len);
 /* GEMM tiling override for experiments and split-K parity tests: pair = -1 auto, 0 single-CTA
  * tiles, 1 CTA-pair tiles, 2 narrow 128 x 128 tiles (residual / QKV epilogues); splits = 0
  * auto, S >= 1 forces S K-slices on the partial-wave tiles (clamped so the split units fit one

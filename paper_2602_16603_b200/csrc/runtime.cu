@@ -1803,6 +1803,110 @@ int fp_op_gemm(fp_ctx* c, int32_t epi, const void* A, const void* B, void* C, in
   return FP_OK;
 }
 
+int fp_op_gate_up_swiglu(fp_ctx* c, const void* x, const void* w_gate, const void* w_up,
+                         void* out, int32_t M, int32_t F, int32_t K) {
+  REQ(c && x && w_gate && w_up && out, "null argument");
+  REQ(M >= 1 && F % 128 == 0 && K % 64 == 0, "gate_up: F%128 and K%64 required");
+  CK(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  // pack [g(128) | u(128)] per 256-row block, the layout of the model's gate/up weights
+  __nv_bfloat16* w = nullptr;
+  CK(cudaMallocAsync((void**)&w, (size_t)2 * F * K * 2, c->stream));
+  for (int half = 0; half < 2; ++half)
+    CK(cudaMemcpy2DAsync(w + (size_t)half * 128 * K, (size_t)256 * K * 2, half ? w_up : w_gate,
+                         (size_t)128 * K * 2, (size_t)128 * K * 2, (size_t)(F / 128),
+                         cudaMemcpyDeviceToDevice, c->stream));
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_map(&ta, x, M, K, 128)) || (rc = make_map(&tb, w, 2 * F, K, 128))) {
+    cudaFreeAsync(w, c->stream);
+    return rc;
+  }
+  GemmParams p{};
+  p.M = M;
+  p.N = 2 * F;
+  p.K = K;
+  p.out = out;
+  p.ldo = F;
+  launch_gemm<EPI_SWIGLU>(c, ta, tb, p, c->stream);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(w, c->stream));
+  return FP_OK;
+}
+
+int fp_op_attn_prefill(fp_ctx* c, const void* q, const void* k, const void* v, void* out,
+                       int32_t n_q, int32_t kv_len) {
+  REQ(c && q && k && v && out, "null argument");
+  REQ(n_q >= 1 && kv_len >= n_q, "attn: need 1 <= n_q <= kv_len");
+  REQ(c->tp_size == 1, "attn op: single-rank contexts only");
+  CK(cudaSetDevice(c->device));
+  const int PS = c->page_size, H = c->hkv, npages = (kv_len + PS - 1) / PS;
+  std::vector<int> pages;
+  {
+    std::lock_guard<std::mutex> lk(c->page_mu);
+    REQ((int)c->free_pages.size() >= npages, "KV page pool exhausted");
+    for (int i = 0; i < npages; ++i) {
+      pages.push_back(c->free_pages.back());
+      c->free_pages.pop_back();
+    }
+  }
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  cudaStream_t st = c->stream;
+  // K / V rows [kv_len, H * 128] into layer 0's pages: [page][k|v][head][slot][128]
+  for (int pg = 0; pg < npages; ++pg) {
+    const int rows = std::min(PS, kv_len - pg * PS);
+    for (int kv = 0; kv < 2; ++kv)
+      for (int h = 0; h < H; ++h) {
+        __nv_bfloat16* dst = c->kv + (((long long)pages[pg] * 2 + kv) * H + h) * PS * 128;
+        const char* src = static_cast<const char*>(kv ? v : k) +
+                          ((long long)pg * PS * H * 128 + (long long)h * 128) * 2;
+        CK(cudaMemcpy2DAsync(dst, 256, src, (size_t)H * 256, 256, rows, cudaMemcpyDeviceToDevice,
+                             st));
+      }
+  }
+  // the query rows are the request's last n_q tokens (prefix = kv_len - n_q)
+  std::vector<AttnTile> items;
+  for (int r0 = 0; r0 < n_q; r0 += 128)
+    items.push_back({r0, std::min(128, n_q - r0), kv_len - n_q + r0, 0});
+  std::stable_sort(items.begin(), items.end(), [](const AttnTile& a, const AttnTile& b) {
+    return a.q_pos0 + a.n_rows > b.q_pos0 + b.n_rows;
+  });
+  const size_t bytes = items.size() * sizeof(AttnTile) + pages.size() * 4;
+  char* meta = nullptr;
+  CK(cudaMallocAsync((void**)&meta, bytes, st));
+  CK(cudaMemcpyAsync(meta, items.data(), items.size() * sizeof(AttnTile), cudaMemcpyHostToDevice,
+                     st));
+  CK(cudaMemcpyAsync(meta + items.size() * sizeof(AttnTile), pages.data(), pages.size() * 4,
+                     cudaMemcpyHostToDevice, st));
+  CUtensorMap tq;
+  int rc = make_map(&tq, q, n_q, c->qdim, 128);
+  if (rc == FP_OK) {
+    AttnTcParams a{};
+    a.items = reinterpret_cast<const AttnTile*>(meta);
+    a.n_items = (int)items.size();
+    a.n_heads = c->hq;
+    a.n_kv_heads = c->hkv;
+    a.pairs_per_kv = (c->hq / c->hkv + 1) / 2;
+    a.out = static_cast<__nv_bfloat16*>(out);
+    a.ldo = c->qdim;
+    a.block_table = reinterpret_cast<const int*>(meta + items.size() * sizeof(AttnTile));
+    a.bt_stride = npages;
+    a.kv_row_layer = 0;
+    a.kv_rows_per_page = 2 * H * PS;
+    a.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
+    a.sched = c->attn_sched;
+    launch_attn(c, tq, c->tm_kv, a, st);
+  }
+  CK(cudaFreeAsync(meta, st));
+  CK(cudaStreamSynchronize(st));
+  {
+    std::lock_guard<std::mutex> lk2(c->page_mu);
+    for (int pg : pages) c->free_pages.push_back(pg);
+  }
+  CK(cudaGetLastError());
+  return rc;
+}
+
 int fp_op_rmsnorm(fp_ctx* c, const void* x, const void* gamma, void* out, int32_t M, int32_t d,
                   float eps) {
   REQ(c && x && gamma && out, "null argument");

@@ -123,3 +123,70 @@ def test_gemm_narrow_tiles(ctx, M, N, K):
         ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
     err = (out.float() - ref).abs().max().item()
     assert err <= 2 ** -7 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("M,F,K", [(1, 128, 64), (300, 512, 512), (4096, 1536, 512),
+                                   (77, 14336 // 4, 4096)])
+def test_gate_up_swiglu(ctx, M, F, K):
+    """gate_up GEMM + SwiGLU epilogue vs torch fp32: silu(x Wg^T) * (x Wu^T)."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(M + F + K)
+    x = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    wg = torch.randn(F, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    wu = torch.randn(F, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    out = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    _lib.check(ctx.lib.fp_op_gate_up_swiglu(ctx.h, x.data_ptr(), wg.data_ptr(), wu.data_ptr(),
+                                            out.data_ptr(), M, F, K))
+    ctx.sync()
+    xf = x.float()
+    ref = torch.nn.functional.silu(xf @ wg.float().t()) * (xf @ wu.float().t())
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2 ** -7 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("n_q,kv_len", [(1, 1), (37, 37), (128, 128), (200, 200), (130, 700),
+                                        (1000, 1000), (64, 4096), (513, 2049)])
+def test_attn_prefill_vs_torch(n_q, kv_len):
+    """Causal prefill attention (tcgen05, paged K/V, GQA) vs torch fp32 attention with the
+    query rows at positions kv_len - n_q ... kv_len - 1 (a chunk share after its prefix)."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    shape = SHAPES["llama3-8b"]  # 32 query heads, 8 KV heads (GQA group 4)
+    c = _attn_ctx(shape)
+    hq, hkv = shape.n_heads, shape.n_kv_heads
+    g = torch.Generator(device="cuda").manual_seed(n_q * 7 + kv_len)
+    q = torch.randn(n_q, hq * 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    k = torch.randn(kv_len, hkv * 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    v = torch.randn(kv_len, hkv * 128, device="cuda", dtype=torch.bfloat16, generator=g)
+    out = torch.empty(n_q, hq * 128, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    _lib.check(c.lib.fp_op_attn_prefill(c.h, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                        out.data_ptr(), n_q, kv_len))
+    qf = q.float().view(n_q, hq, 128).transpose(0, 1)
+    kf = k.float().view(kv_len, hkv, 128).transpose(0, 1).repeat_interleave(hq // hkv, 0)
+    vf = v.float().view(kv_len, hkv, 128).transpose(0, 1).repeat_interleave(hq // hkv, 0)
+    pos = torch.arange(kv_len - n_q, kv_len, device="cuda")[:, None]
+    mask = torch.arange(kv_len, device="cuda")[None, :] <= pos
+    ref = torch.nn.functional.scaled_dot_product_attention(qf, kf, vf, attn_mask=mask)
+    ref = ref.transpose(0, 1).reshape(n_q, hq * 128)
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item(), err
+
+
+_ATTN = {}
+
+
+def _attn_ctx(shape):
+    from paper_2602_16603_b200.native import PrefillContext
+
+    if "c" not in _ATTN:  # one context (weights are never touched by the op)
+        _ATTN["c"] = PrefillContext(shape, kv_pages=64, page_size=128, max_pos=8192)
+    return _ATTN["c"]
