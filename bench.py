@@ -162,6 +162,22 @@ def cpu_sample(shape_name: str = MODEL, n_tokens: int = 512, reps: int = 1):
     return tok_s, cores, f"1 layer x {n_tokens} tokens of {shape_name} (fp32 numpy), x{full.num_layers} layers"
 
 
+def control_plane_time(duration: float = 60.0, rate: float = 20.0):
+    """SURVEY 8(d) CPU timing (1): wall time of the reference's own run() (scheduler + event
+    engine, virtual clock, default cost model) on the config-2 trace, one host core."""
+    from paper_2602_16603_b200 import refsim
+
+    ps = refsim.load()
+    tr = config2_trace(rate=rate, duration=duration)
+    t0 = time.perf_counter()
+    res = ps.run(tr, ps.PolicyConfig(), ps.CostParams(), 0)
+    wall = time.perf_counter() - t0
+    return {"requests": len(tr), "rounds": res.rounds, "wall_s": round(wall, 3),
+            "us_per_round": round(wall / max(res.rounds, 1) * 1e6, 1),
+            "what": f"reference prefillsim.run() on {duration:.0f} s of the config-2 trace at "
+                    f"{rate:g} req/s (S-EDF, operator), 1 core"}
+
+
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -389,7 +405,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:
         v, cores, sample = cpu_sample()
-        cpu = {"value": v, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample}
+        cpu = {"value": v, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample,
+               "control_plane": control_plane_time()}
 
     for t in tasks:
         t.destroy()
