@@ -214,7 +214,10 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           ws = 0;
           wph ^= 1;
         }
-        if (w < 0) break;
+        if (w < 0) {
+          grid_dep_launch();  // no more work for this CTA: the next kernel may start its prologue
+          break;
+        }
         const AttnWork a = attn_decode(p, w);
         const int* bt = p.block_table + (long long)a.it.req * p.bt_stride;
         mbar_wait(q_empty, (it & 1) ^ 1);  // the previous item's last QK^T has run

@@ -296,6 +296,11 @@ DEVI uint4 ld_cg_v4(const void* p) {
 // Programmatic dependent launch: wait until the preceding kernel in the stream has completed
 // and its memory is visible (no-op when the launch was not programmatic).
 DEVI void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next kernel in the stream be scheduled (its prologue runs on SMs this grid no longer
+// needs; its griddepcontrol.wait still waits for this grid to complete). Takes effect once
+// every CTA of this grid has issued it or exited, so all of this grid's CTAs are resident by
+// then and the early launch cannot starve them of SMs.
+DEVI void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 DEVI float fast_exp2(float x) {
   float y;

@@ -580,6 +580,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
+    if (lane == 0) grid_dep_launch();  // all loads issued: the next kernel may start its prologue
   } else if (warp == 1 && leader) {
     constexpr uint32_t idesc = make_idesc_bf16(Cfg::TILE_M, BN);
     int s = 0;
