@@ -224,6 +224,7 @@ struct fp_ctx {
   int* attn_sched = nullptr;  // persistent attention work counter (self-resetting)
   unsigned long long* gemm_dbg = nullptr;  // FP_GEMM_STAMPS=1: phase stamps of fp_op_gemm launches
   bool use_pair_gemm = true;
+  bool use_narrow = true;  // FP_NARROW=0: never 128 x 128 tiles (experiments)
   int force_splits = 0;   // FP_FORCE_SPLITS (experiments)
   int force_pair = -1;    // FP_FORCE_PAIR (experiments): 0 single, 1 pair
 };
@@ -305,8 +306,9 @@ static constexpr double kSplitOverheadKbQkv = 60.0;  // RoPE / KV-scatter items 
 static bool split_tail_ok(int epi, int K) {
   return epi != EPI_QKV && epi != EPI_SWIGLU && K / kGemmBK >= 128;
 }
+static double g_split_ov_scale = 1.0;  // FP_SPLIT_OV_SCALE (experiments)
 static double split_overhead(int epi) {
-  return epi == EPI_QKV ? kSplitOverheadKbQkv : kSplitOverheadKb;
+  return g_split_ov_scale * (epi == EPI_QKV ? kSplitOverheadKbQkv : kSplitOverheadKb);
 }
 static double choose_splits(int tiles, int num_k, int num_sms, int* full_tiles, int* splits,
                             bool tail_ok = true, double overhead = kSplitOverheadKb) {
@@ -433,7 +435,7 @@ static bool pick_pair(const fp_ctx* c, int epi, int M, int N, int K) {
 // chosen when it beats the best 256-wide plan by 10%.
 static constexpr double kNarrowKbCost = 0.8;
 static bool pick_narrow(const fp_ctx* c, int epi, int M, int N, int K) {
-  if (epi != EPI_RESID && epi != EPI_QKV) return false;
+  if ((epi != EPI_RESID && epi != EPI_QKV) || !c->use_narrow) return false;
   if (c->force_pair == 2) return true;
   if (c->force_pair >= 0 || c->force_splits > 0) return false;
   const int num_k = K / kGemmBK, nN = N / 256;
@@ -959,6 +961,8 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   CK(cudaMemset(c->kv, 0, (size_t)L * kv_pages * c->page_elems * 2));
   {
     if (const char* e = getenv("FP_PAIR_GEMM")) c->use_pair_gemm = atoi(e) != 0;
+    if (const char* e = getenv("FP_NARROW")) c->use_narrow = atoi(e) != 0;
+    if (const char* e = getenv("FP_SPLIT_OV_SCALE")) g_split_ov_scale = atof(e);
     if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
     if (const char* e = getenv("FP_TP_FUSED")) c->tp_fused = atoi(e) != 0;
