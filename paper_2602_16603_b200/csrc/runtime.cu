@@ -161,7 +161,7 @@ struct Task {
   __nv_bfloat16 *xperm = nullptr, *actp = nullptr, *yperm = nullptr;
   CUtensorMap tm_xperm, tm_actp;
   int moe_rows = 0;                            // rows of the current chunk's routing
-  cudaEvent_t ready, done;
+  cudaEvent_t ready, done, fence;  // fence: after the last launch that touches the task
   // host execution state
   int gen = 0, seg_first = 0, enq = 0, seg_ack0 = 0, done_recorded = 0;
   std::atomic<int> worker_active{0};
@@ -176,6 +176,7 @@ struct fp_ctx {
   int qdim = 0, kvdim = 0, qkv_n = 0, vocab_pad = 0;
   int tp_rank = 0, tp_size = 1;
   cudaStream_t stream = nullptr, upload = nullptr, readback = nullptr;
+  cudaStream_t release = nullptr;  // task frees, each behind its own task's last launch only
   cudaStream_t own_stream = nullptr;  // lock-step TP groups share rank 0's stream
   // tensor parallel exchange (null when tp_size == 1)
   TpDev tp_host{};
@@ -304,7 +305,7 @@ static constexpr double kSplitOverheadKbQkv = 60.0;  // RoPE / KV-scatter items 
 // Tails behind full waves split only for long K (down_proj): the split-capable instantiation
 // runs the full-wave tiles with more register pressure (measured slower for QKV / SwiGLU).
 static bool split_tail_ok(int epi, int K) {
-  return epi != EPI_QKV && epi != EPI_SWIGLU && K / kGemmBK >= 128;
+  return epi != EPI_QKV && epi != EPI_SWIGLU && epi != EPI_STORE_F32 && K / kGemmBK >= 128;
 }
 static double g_split_ov_scale = 1.0;  // FP_SPLIT_OV_SCALE (experiments)
 static double split_overhead(int epi) {
@@ -348,7 +349,8 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   const int slots = c->num_sms / CG;  // concurrent tiles (CTA pairs)
   p.splits = 1;
   p.full_tiles = tiles;
-  if (c->ws && EPI != EPI_STORE_F32 && BN == 256)
+  // fp32 stores (lm_head, MoE router) split only when all their tiles do (no full wave)
+  if (c->ws && BN == 256)
     choose_splits(tiles, p.K / kGemmBK, slots, &p.full_tiles, &p.splits, split_tail_ok(EPI, p.K),
                   split_overhead(EPI));
   if (p.xchg) {  // TP exchange GEMMs publish / fold their partials per tile: never split
@@ -821,6 +823,7 @@ static void worker_main(fp_ctx* c) {
     {
       std::lock_guard<std::mutex> lk(c->launch_mu);
       cudaEventRecord(t->done, c->stream);
+      cudaEventRecord(t->fence, c->stream);
       t->done_recorded = 1;
     }
     {
@@ -883,6 +886,7 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   c->own_stream = c->stream;
   CK(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->readback, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->release, cudaStreamNonBlocking));
   // let the async mempool keep freed task workspaces
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -984,6 +988,22 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   memset((void*)c->hctl, 0, sizeof(HostCtl));
   c->hctl->progress_task = -1;
   CK(cudaHostGetDevicePointer((void**)&c->dctl, (void*)c->hctl, 0));
+  // Pre-grow the (shared, never-trimmed) async pool that task workspaces come from: growing it
+  // maps physical memory inside cudaMallocAsync, which blocks task creation while the GPU runs
+  // (measured: up to ~5 ms per task in a serving loop). FP_POOL_RESERVE_MB overrides the
+  // default of 8 GB (capped at a quarter of the free memory); 0 disables.
+  {
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    size_t reserve = std::min<size_t>((size_t)8 << 30, free_b / 4);
+    if (const char* e = getenv("FP_POOL_RESERVE_MB")) reserve = (size_t)atoll(e) << 20;
+    if (reserve > 0) {
+      void* r = nullptr;
+      CK(cudaMallocAsync(&r, reserve, c->upload));
+      CK(cudaFreeAsync(r, c->upload));
+      CK(cudaStreamSynchronize(c->upload));
+    }
+  }
   c->worker = std::thread(worker_main, c);
   *out = c;
   return FP_OK;
@@ -1033,6 +1053,7 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaStreamDestroy(c->own_stream);
   cudaStreamDestroy(c->upload);
   cudaStreamDestroy(c->readback);
+  cudaStreamDestroy(c->release);
   delete c;
   return FP_OK;
 }
@@ -1507,6 +1528,8 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   CK(cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming));
   CK(cudaEventRecord(t->ready, up));
   CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&t->fence, cudaEventDisableTiming));
+  CK(cudaEventRecord(t->fence, up));
   *out = reinterpret_cast<fp_task*>(t);
   return FP_OK;
 }
@@ -1546,11 +1569,15 @@ int fp_task_destroy(fp_ctx* c, fp_task* task) {
   REQ(c, "null ctx");
   CK(cudaSetDevice(c->device));
   while (t->worker_active.load()) std::this_thread::yield();
-  // stream-ordered frees behind any queued (no-op) launches of this task
-  cudaStream_t st = c->stream;
+  // Stream-ordered frees behind this task's last launch (t->fence: queued no-op launches of a
+  // stopped segment included), on a stream of their own: freed on the prefill stream they
+  // would wait for every task enqueued after this one, and the pool would make the next task's
+  // allocations (upload stream) wait for those too.
+  cudaStream_t st = c->release;
   {
     std::lock_guard<std::mutex> lk(c->launch_mu);
     cudaStreamWaitEvent(st, t->ready, 0);
+    cudaStreamWaitEvent(st, t->fence, 0);
     cudaFreeAsync(t->meta, st);
     cudaFreeAsync(t->h, st);
     cudaFreeAsync(t->ssq, st);
@@ -1568,6 +1595,7 @@ int fp_task_destroy(fp_ctx* c, fp_task* task) {
   }
   cudaEventDestroy(t->ready);
   cudaEventDestroy(t->done);
+  cudaEventDestroy(t->fence);
   {
     std::lock_guard<std::mutex> lk(c->page_mu);
     for (int p : t->pages) c->free_pages.push_back(p);
@@ -1593,6 +1621,7 @@ int fp_task_begin_segment(fp_ctx* c, fp_task* task, int32_t first) {
   t->seg_ack0 = c->hctl->ack_seq;
   CK(cudaStreamWaitEvent(c->stream, t->ready, 0));
   CK(cudaMemsetAsync(&t->ctl->dec[first], 0, (size_t)(t->n_entries - first) * 4, c->stream));
+  CK(cudaEventRecord(t->fence, c->stream));
   return FP_OK;
 }
 
@@ -1611,6 +1640,7 @@ int fp_task_enqueue(fp_ctx* c, fp_task* task, int32_t first, int32_t last) {
     CK(cudaEventRecord(t->done, c->stream));
     t->done_recorded = 1;
   }
+  CK(cudaEventRecord(t->fence, c->stream));
   CK(cudaGetLastError());
   return FP_OK;
 }
@@ -2075,6 +2105,7 @@ int fp_tp_enqueue_lockstep(fp_ctx** ctxs, fp_task** tasks, int32_t n, int32_t fi
       CK(cudaEventRecord(ts[r]->done, ctxs[r]->stream));
       ts[r]->done_recorded = 1;
     }
+    CK(cudaEventRecord(ts[r]->fence, ctxs[r]->stream));
   }
   CK(cudaGetLastError());
   return FP_OK;
