@@ -249,7 +249,8 @@ int fp_op_gate_up_swiglu(fp_ctx* ctx, const void* x, const void* w_gate, const v
 int fp_op_attn_prefill(fp_ctx* ctx, const void* q, const void* k, const void* v, void* out,
                        int32_t n_q, int32_t kv_len);
 /* GEMM tiling override for experiments and split-K parity tests: pair = -1 auto, 0 single-CTA
- * tiles, 1 CTA-pair tiles, 2 narrow 128 x 128 tiles (residual / QKV epilogues); splits = 0
+ * tiles, 1 CTA-pair tiles, 2 narrow 128 x 128 tiles (residual / QKV epilogues), 3 stream-K
+ * (whole tiles, then equal (tile, k-block) ranges per CTA); splits = 0
  * auto, S >= 1 forces S K-slices on the partial-wave tiles (clamped so the split units fit one
  * round of the persistent grid). */
 int fp_ctx_set_gemm_policy(fp_ctx* ctx, int32_t pair, int32_t splits);

@@ -77,6 +77,13 @@ struct GemmParams {
   const int* grp_off;     // [E + 1] expert row offsets (live-row bound)
   const int* grp_perm;    // [rows] token of each row (fused-norm lookup)
   int grp_b_rows;         // B rows per expert
+  // MODE 3 (stream-K): full_tiles = whole tiles processed first (round-robin), the rest of the
+  // (tile, k-block) space is cut into gridDim.x equal contiguous ranges; sk_flags[cta] =
+  // sk_epoch once that CTA's partial tile is in the workspace
+  int* sk_flags;
+  int sk_epoch;
+  int group_m;  // m-blocks per raster group (0: kGemmGroupM); the launcher sets "all" when the
+                // whole A operand fits in L2, so every weight tile is read from HBM once
   Guard guard;
 };
 
@@ -110,14 +117,16 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int TILE_M = kGemmBM * CG;
   static constexpr int SMEM_BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+  // stream-K: + two 16 KB buffers for the partner partials of a finishing tile
+  static constexpr int SK_SMEM_BYTES = SMEM_BYTES + 2 * 16384;
 };
 
-DEVI void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = kGemmGroupM * num_n;
+DEVI void tile_coords(int t, int num_m, int num_n, int group, int& mb, int& nb) {
+  const int per_group = group * num_n;
   const int g = t / per_group;
-  const int first_m = g * kGemmGroupM;
+  const int first_m = g * group;
   int gm = num_m - first_m;
-  if (gm > kGemmGroupM) gm = kGemmGroupM;
+  if (gm > group) gm = group;
   const int local = t - g * per_group;
   mb = first_m + local % gm;
   nb = local / gm;
@@ -463,6 +472,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* pbar = tempty + 3;  // MODE 3: partner-partial buffers' barriers [2]
+  uint8_t* sPart = sB + STAGES * Cfg::B_BYTES + 256;  // MODE 3: 2 x 16 KB
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -481,6 +492,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);  // one arrival per epilogue warp of every CTA
+      if constexpr (MODE == 3) mbar_init(&pbar[a], 1);
     }
     fence_barrier_init();
   }
@@ -527,18 +539,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       kb1 = min(num_k, kb0 + per);
     }
   };
+  // MODE 3 (stream-K). This CTA's range [sk_s, sk_e) of the stream-K (tile, k-block) space
+  // (tiles after the full_tiles whole ones, k fastest) runs as: first the partial of the tile
+  // its range ends inside (if any: published to the workspace at once, so no CTA ever waits on
+  // a chain), then every tile that finishes inside the range -- the first of them, if the
+  // range starts inside it, takes the partials of the CTAs before it (its "partners").
+  const int dp_tiles = MODE == 3 ? min(p.full_tiles, num_tiles) : 0;
+  const long long sk_u = MODE == 3 ? (long long)(num_tiles - dp_tiles) * num_k : 0;
+  const int sk_g = gridDim.x;
+  const int sk_s = MODE == 3 ? (int)((long long)blockIdx.x * sk_u / sk_g) : 0;
+  const int sk_e = MODE == 3 ? (int)((long long)(blockIdx.x + 1) * sk_u / sk_g) : 0;
+  const int sk_dp_mine = (MODE == 3 && (int)blockIdx.x < dp_tiles)
+                             ? (dp_tiles - 1 - (int)blockIdx.x) / sk_g + 1 : 0;
+  const int sk_prod = (MODE == 3 && sk_e > sk_s && sk_e % num_k != 0) ? 1 : 0;
+  const int sk_t0 = num_k > 0 ? sk_s / num_k : 0;
+  const int sk_fin = MODE == 3 ? max(0, (num_k > 0 ? sk_e / num_k : 0) - sk_t0) : 0;
+  const int n_work = !run ? 0
+                     : MODE == 3 ? sk_dp_mine + sk_prod + sk_fin
+                                 : (unit0 < num_units ? (num_units - unit0 + unit_step - 1) / unit_step : 0);
+  // work item -> (tile, K-slice, slices, k-blocks, role: 0 whole / finishing without partners,
+  // 1 stream-K partial producer, 2 stream-K finisher with partners)
+  auto work_info = [&](int w, int& tile, int& split, int& nsplit, int& kb0, int& kb1, int& role) {
+    role = 0;
+    if constexpr (MODE == 3) {
+      split = 0;
+      nsplit = 1;
+      if (w < sk_dp_mine) {
+        tile = (int)blockIdx.x + w * sk_g;
+        kb0 = 0;
+        kb1 = num_k;
+        return;
+      }
+      w -= sk_dp_mine;
+      int t;
+      if (w < sk_prod) {
+        t = sk_e / num_k;
+        kb1 = sk_e - t * num_k;
+        role = 1;
+      } else {
+        t = sk_t0 + (w - sk_prod);
+        kb1 = num_k;
+      }
+      kb0 = max(sk_s - t * num_k, 0);
+      if (role == 0 && kb0 > 0) role = 2;
+      tile = dp_tiles + t;
+    } else {
+      unit_info(unit0 + w * unit_step, tile, split, nsplit, kb0, kb1);
+    }
+  };
   // tile -> (m-block, n-block, first A row, first B row, end of live rows)
   auto tile_geom = [&](int tile, int& mb, int& nb, int& row_a, int& row_b, int& row_end) {
     if constexpr (MODE == 2) {
       int mt;
-      tile_coords(tile, num_m, num_n, mt, nb);
+      tile_coords(tile, num_m, num_n, kGemmGroupM, mt, nb);
       const int2 te = reinterpret_cast<const int2*>(p.grp_mtiles)[mt];
       mb = mt;
       row_a = te.y;
       row_b = te.x * p.grp_b_rows + nb * BN;
       row_end = p.grp_off[te.x + 1];
     } else {
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords(tile, num_m, num_n, p.group_m > 0 ? p.group_m : kGemmGroupM, mb, nb);
       row_a = mb * Cfg::TILE_M + (int)rank * kGemmBM;
       row_b = nb * BN + (int)rank * (BN / CG);
       row_end = p.M;
@@ -549,9 +609,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint64_t pol_b = policy_evict_last();
     int s = 0;
     uint32_t ph = 0;
-    for (int u = unit0; u < num_units; u += unit_step) {
-      int tile, split, nsplit, kb0, kb1;
-      unit_info(u, tile, split, nsplit, kb0, kb1);
+    for (int w = 0; w < n_work; ++w) {
+      int tile, split, nsplit, kb0, kb1, role;
+      work_info(w, tile, split, nsplit, kb0, kb1, role);
       int mb, nb, row_a, row_b, row_end;
       tile_geom(tile, mb, nb, row_a, row_b, row_end);
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -559,7 +619,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) {
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
-            if (kb == kb0 && u == unit0) GEMM_STAMP(3);
+            if (kb == kb0 && w == 0) GEMM_STAMP(3);
             tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * kGemmBK, row_a);
 #pragma unroll
             for (int h = 0; h < BN / 128; ++h)  // weight maps use 128-row boxes
@@ -586,9 +646,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
-    for (int u = unit0; u < num_units; u += unit_step, ++it) {
-      int tile, split, nsplit, kb0, kb1;
-      unit_info(u, tile, split, nsplit, kb0, kb1);
+    for (int w = 0; w < n_work; ++w, ++it) {
+      int tile, split, nsplit, kb0, kb1, role;
+      work_info(w, tile, split, nsplit, kb0, kb1, role);
       const int acc = it & 1;
       const uint32_t acc_ph = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_ph ^ 1);
@@ -597,7 +657,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
-        if (lane == 0 && kb == kb0 && u == unit0) GEMM_STAMP(4);
+        if (lane == 0 && kb == kb0 && w == 0) GEMM_STAMP(4);
         if (lane == 0) {
           const uint64_t a0 = make_sdesc_sw128(smem_u32(sA + s * Cfg::A_BYTES), 16, 1024);
           const uint64_t b0 = make_sdesc_sw128(smem_u32(sB + s * Cfg::B_BYTES), 16, 1024);
@@ -643,9 +703,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         else mbar_arrive_cluster(&tempty[acc], 0);
       }
     };
-    for (int u = unit0; u < num_units; u += unit_step, ++it) {
-      int tile, split, splits, kb0, kb1;
-      unit_info(u, tile, split, splits, kb0, kb1);
+    for (int w = 0; w < n_work; ++w, ++it) {
+      int tile, split, splits, kb0, kb1, role;
+      work_info(w, tile, split, splits, kb0, kb1, role);
       int mb, nb, row_a, row_b, row_end;
       tile_geom(tile, mb, nb, row_a, row_b, row_end);
       const int acc = it & 1;
@@ -659,6 +719,90 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       float4* ws_tile =
           reinterpret_cast<float4*>(p.ws) + (long long)wtile * splits * (BN / 4) * kGemmBM;
       const uint32_t tacc = tbase + acc * BN + ((uint32_t)(q * 32) << 16);
+      if constexpr (MODE == 3) {
+        if (role == 1) {
+          // stream-K partial: TMEM -> this CTA's workspace slot ([col/4][row] float4), publish
+          mbar_wait(&tfull[acc], acc_ph);
+          tc_fence_after();
+          float4* dst = reinterpret_cast<float4*>(p.ws) + (long long)blockIdx.x * (BN / 4) * kGemmBM + row;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tacc + c * 32, r);
+            tmem_ld_wait();
+            if (live) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                st_global_v4(dst + (c * 8 + i) * kGemmBM,
+                             make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]));
+            }
+          }
+          release_acc(acc);
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (row == 0) st_release_gpu(p.sk_flags + blockIdx.x, p.sk_epoch);
+          continue;
+        }
+        if (role == 2) {
+          // stream-K finisher: add the partners' partials (k order) into the TMEM accumulator,
+          // 16 KB chunks (32 columns of one partner) double-buffered through shared memory by
+          // bulk copies, then run the ordinary epilogue below
+          mbar_wait(&tfull[acc], acc_ph);
+          tc_fence_after();
+          const long long t0u = (long long)(tile - dp_tiles) * num_k;
+          const int g_lo = (int)(((t0u + 1) * sk_g + sk_u - 1) / sk_u) - 1;
+          const int P = (int)blockIdx.x - g_lo;
+          if (threadIdx.x == 128) {
+            for (int g = g_lo; g < (int)blockIdx.x; ++g)
+              while (ld_acquire_gpu(p.sk_flags + g) != p.sk_epoch) __nanosleep(32);
+            fence_proxy_async_global();
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const float4* wsb = reinterpret_cast<const float4*>(p.ws);
+          const int steps = (BN / 32) * P;
+          auto issue = [&](int step) {  // step = c * P + j: columns [32c, 32c + 32) of partner j
+            const int c = step / P, j = step - c * P;
+            mbar_arrive_expect_tx(&pbar[step & 1], 16384);
+            bulk_g2s(sPart + (step & 1) * 16384, wsb + ((long long)(g_lo + j) * (BN / 4) + c * 8) * kGemmBM,
+                     16384, &pbar[step & 1]);
+          };
+          if (threadIdx.x == 128) {
+            issue(0);
+            if (steps > 1) issue(1);
+          }
+          float v[32];
+#pragma unroll 1
+          for (int step = 0; step < steps; ++step) {
+            const int c = step / P, j = step - c * P;
+            if (j == 0) {
+              uint32_t r[32];
+              tmem_ld32(tacc + c * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            }
+            mbar_wait(&pbar[step & 1], (step >> 1) & 1);
+            const float4* sp = reinterpret_cast<const float4*>(sPart + (step & 1) * 16384) + row;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 f = sp[i * kGemmBM];
+              v[4 * i] += f.x;
+              v[4 * i + 1] += f.y;
+              v[4 * i + 2] += f.z;
+              v[4 * i + 3] += f.w;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // every thread is done with the buffer
+            if (threadIdx.x == 128 && step + 2 < steps) issue(step + 2);
+            if (j == P - 1) {
+              uint32_t r[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
+              tmem_st32(tacc + c * 32, r);
+              tmem_st_wait();
+            }
+          }
+        }
+      }
       if (MODE == 1 && splits > 1) {
         mbar_wait(&tfull[acc], acc_ph);
         if (threadIdx.x == 128) GEMM_STAMP(6);

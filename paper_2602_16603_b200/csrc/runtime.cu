@@ -227,7 +227,13 @@ struct fp_ctx {
   bool use_pair_gemm = true;
   bool use_narrow = true;  // FP_NARROW=0: never 128 x 128 tiles (experiments)
   int force_splits = 0;   // FP_FORCE_SPLITS (experiments)
-  int force_pair = -1;    // FP_FORCE_PAIR (experiments): 0 single, 1 pair
+  int force_pair = -1;    // FP_FORCE_PAIR (experiments): 0 single, 1 pair, 2 narrow, 3 stream-K
+  // FP_STREAMK=1: stream-K where its cost model wins. Off by default: measured neutral on the
+  // power-capped B200 (the idle SMs of a partial wave cost little energy; the partial
+  // round trips add traffic), forced by policy 3 in the parity tests.
+  bool use_streamk = false;
+  int* sk_flags = nullptr;  // stream-K partial flags [num_sms]
+  int sk_epoch = 0;         // per stream-K launch (flags compare against it: no reset)
 };
 
 static cudaEvent_t ev_get(fp_ctx* c) {
@@ -332,6 +338,14 @@ static double choose_splits(int tiles, int num_k, int num_sms, int* full_tiles, 
   return full_cost + best_t;
 }
 
+// Raster group: one group over all m-blocks when the whole A operand fits comfortably in L2
+// (then each weight tile is streamed from HBM once instead of once per 16-m-block group; ncu:
+// gate_up at M = 4465 read 573 MB for 271 MB of operands), else kGemmGroupM.
+static int g_raster_all_mb = 48;  // FP_RASTER_ALL_MB (0 = always kGemmGroupM)
+static int raster_group(const fp_ctx*, const GemmParams& p) {
+  return (long long)p.M * p.K * 2 <= ((long long)g_raster_all_mb << 20) ? (1 << 20) : 0;
+}
+
 template <int EPI, int CG, int BN = 256>
 static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b, GemmParams p,
                            cudaStream_t st) {
@@ -347,6 +361,7 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   }
   const int tiles = ((p.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * (p.N / BN);
   const int slots = c->num_sms / CG;  // concurrent tiles (CTA pairs)
+  p.group_m = raster_group(c, p);
   p.splits = 1;
   p.full_tiles = tiles;
   // fp32 stores (lm_head, MoE router) split only when all their tiles do (no full wave)
@@ -454,9 +469,87 @@ static bool pick_narrow(const fp_ctx* c, int epi, int M, int N, int K) {
   return t128 * 1.1 < t256;
 }
 
+// Stream-K (gemm.cuh MODE 3, 128 x 256 single-CTA tiles): whole tiles for all but the last
+// one-to-two waves, then the remaining (tile, k-block) space cut into one equal contiguous range
+// per CTA -- no wave quantisation, no idle SMs for under-filled launches. Cost in k-block units:
+// the range, pipeline fill, the partial store / flag (kSkFixKb) and, per partner partial a
+// finishing tile folds in, one 128 KB bulk read (kSkPartnerKb).
+static constexpr double kSkFixKb = 6.0;
+// One partner partial = 8 serial 16 KB bulk round trips through the 2 shared-memory buffers
+// (~1 us each): measured ~20 k-block equivalents. Launches whose tiles do not fill the machine
+// (every tile would need several partners) keep split-K / narrow tiles instead.
+static constexpr double kSkPartnerKb = 20.0;
+static constexpr int kSkMinKb = 8;  // k-blocks per CTA at least (bounds the partners per tile)
+static double g_sk_fix_scale = 1.0;  // FP_SK_FIX_SCALE (experiments)
+struct SkPlan {
+  int dp_tiles = 0, grid = 0;
+  double cost = 1e30;
+};
+static SkPlan plan_streamk(const fp_ctx* c, int M, int N, int K) {
+  SkPlan pl;
+  const int T = ((M + kGemmBM - 1) / kGemmBM) * (N / 256), nk = K / kGemmBK, G0 = c->num_sms;
+  const int waves = T / G0;
+  if (waves < 1 && c->force_pair != 3) return pl;  // at most one partner per tile
+  pl.dp_tiles = waves >= 2 ? (waves - 1) * G0 : 0;
+  const long long U = (long long)(T - pl.dp_tiles) * nk;
+  pl.grid = (int)std::min<long long>(G0, U / kSkMinKb);
+  if (pl.grid < 2) return pl;
+  const double per = std::ceil((double)U / pl.grid);
+  const double partners = std::ceil(nk / per);
+  pl.cost = (double)(pl.dp_tiles / G0) * (nk + 4.0) + per + 4.0 +
+            g_sk_fix_scale * (kSkFixKb + kSkPartnerKb * partners);
+  return pl;
+}
+
+template <int EPI>
+static void launch_gemm_sk(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b, GemmParams p,
+                           cudaStream_t st, const SkPlan& pl) {
+  using Cfg = GemmCfg<256, 1>;
+  auto kern = gemm_bf16_tn_kernel<256, EPI, 1, 3>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SK_SMEM_BYTES);
+    attr = true;
+  }
+  p.splits = 1;
+  p.full_tiles = pl.dp_tiles;
+  p.group_m = raster_group(c, p);
+  p.ws = c->ws;
+  p.tickets = c->tickets;
+  p.sk_flags = c->sk_flags;
+  p.sk_epoch = ++c->sk_epoch;
+  launch_pdl(kern, dim3(pl.grid), dim3(kGemmThreads), Cfg::SK_SMEM_BYTES, st, a, b, p);
+}
+
+// Cost (k-block units) of the best plan among single-CTA / pair / narrow tiles, as the pickers
+// below see it.
+static double plan_cost_tiled(const fp_ctx* c, int epi, int M, int N, int K) {
+  int ft, sp;
+  const int nN = N / 256, num_k = K / kGemmBK;
+  const bool tail = split_tail_ok(epi, K);
+  const double ov = split_overhead(epi);
+  double t = choose_splits(((M + 127) / 128) * nN, num_k, c->num_sms, &ft, &sp, tail, ov);
+  if (c->use_pair_gemm && M > kGemmBM)
+    t = std::min(t, choose_splits(((M + 255) / 256) * nN, num_k, c->num_sms / 2, &ft, &sp, tail,
+                                  ov) / 1.09);
+  if ((epi == EPI_RESID || epi == EPI_QKV) && c->use_narrow) {
+    const long long tiles = (long long)((M + 127) / 128) * (N / 128);
+    t = std::min(t, std::ceil((double)tiles / c->num_sms) * (kNarrowKbCost * num_k + 4.0));
+  }
+  return t;
+}
+
 template <int EPI>
 static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
                         const GemmParams& p, cudaStream_t st) {
+  if (!p.xchg && (c->force_pair == 3 || (c->use_streamk && c->force_pair < 0 && c->force_splits == 0))) {
+    const SkPlan pl = plan_streamk(c, p.M, p.N, p.K);
+    if (pl.grid >= 2 &&
+        (c->force_pair == 3 || pl.cost < 0.92 * plan_cost_tiled(c, EPI, p.M, p.N, p.K))) {
+      launch_gemm_sk<EPI>(c, a, b, p, st, pl);
+      return;
+    }
+  }
   if constexpr (EPI == EPI_RESID || EPI == EPI_QKV) {
     if (!p.xchg && pick_narrow(c, EPI, p.M, p.N, p.K)) {
       launch_gemm_cg<EPI, 1, 128>(c, a, b, p, st);
@@ -966,6 +1059,9 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   {
     if (const char* e = getenv("FP_PAIR_GEMM")) c->use_pair_gemm = atoi(e) != 0;
     if (const char* e = getenv("FP_NARROW")) c->use_narrow = atoi(e) != 0;
+    if (const char* e = getenv("FP_STREAMK")) c->use_streamk = atoi(e) != 0;
+    if (const char* e = getenv("FP_RASTER_ALL_MB")) g_raster_all_mb = atoi(e);
+    if (const char* e = getenv("FP_SK_FIX_SCALE")) g_sk_fix_scale = atof(e);
     if (const char* e = getenv("FP_SPLIT_OV_SCALE")) g_split_ov_scale = atof(e);
     if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
@@ -983,6 +1079,8 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   CK(cudaMalloc(&c->attn_sched, 2 * sizeof(int)));
   CK(cudaMemset(c->attn_sched, 0, 2 * sizeof(int)));
   CK(cudaMalloc(&c->tickets, 4096 * sizeof(int)));
+  CK(cudaMalloc(&c->sk_flags, (size_t)c->num_sms * sizeof(int)));
+  CK(cudaMemset(c->sk_flags, 0, (size_t)c->num_sms * sizeof(int)));
   CK(cudaMemset(c->tickets, 0, 4096 * sizeof(int)));
   CK(cudaHostAlloc(&c->hctl, sizeof(HostCtl), cudaHostAllocMapped));
   memset((void*)c->hctl, 0, sizeof(HostCtl));
@@ -1083,7 +1181,7 @@ int fp_debug_gemm_stamps(fp_ctx* c, uint64_t* out, int32_t max_ctas) {
   return FP_OK;
 }
 int fp_ctx_set_gemm_policy(fp_ctx* c, int32_t pair, int32_t splits) {
-  REQ(c && pair >= -1 && pair <= 2 && splits >= 0 && splits <= 32, "bad gemm policy");
+  REQ(c && pair >= -1 && pair <= 3 && splits >= 0 && splits <= 32, "bad gemm policy");
   c->force_pair = pair;
   c->force_splits = splits;
   return FP_OK;

@@ -167,10 +167,12 @@ def test_qwen_variants_vs_hf_and_oracle(golden_dir, name):
     ctx.close()
 
 
-@pytest.mark.parametrize("policy", [2, 0])
+@pytest.mark.parametrize("policy", [2, 0, 3])
 def test_forced_gemm_tiling_vs_oracle(tiny, policy):
     """Every GEMM of the forward with narrow 128 x 128 tiles (policy 2: residual and QKV
-    epilogues) or single-CTA 256-wide tiles (policy 0): logits and KV within tolerance."""
+    epilogues), single-CTA 256-wide tiles (policy 0) or stream-K (policy 3: every epilogue,
+    the fused norm applied after the partner partials are folded in): logits and KV within
+    tolerance."""
     shape, w, ctx = tiny
     tokens = F.make_tokens([37, 300, 130], shape.vocab, 21)
     ot = F.OracleTask(shape, w, tokens, None)

@@ -125,9 +125,50 @@ def test_gemm_narrow_tiles(ctx, M, N, K):
     assert err <= 2 ** -7 * ref.abs().max().item() + 1e-3, err
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 256, 1024), (42, 4096, 4096), (300, 1024, 4096),
+                                   (77, 4096, 14336), (2000, 4096, 4096), (4096, 6144, 4096),
+                                   (5000, 4096, 1024)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_streamk(ctx, M, N, K, epi):
+    """Stream-K (policy 3): whole tiles first, then equal contiguous (tile, k-block) ranges per
+    CTA; a tile's finishing CTA folds its partners' partials into TMEM. Covers all-stream-K
+    launches with up to ~8 partners per tile, one-to-two-wave launches, and whole-tile waves in
+    front. Within bf16 tolerance of fp32 and bit-identical run to run."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + epi + 3)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    if epi == 1:
+        R = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    else:
+        R = torch.randn(M, N, device="cuda", dtype=torch.bfloat16, generator=g)
+    ref = A.float() @ B.float().t() + (R.float() if epi == 2 else 0.0)
+    outs = []
+    try:
+        _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, 3, 0))
+        for _ in range(2):
+            out = R.clone()
+            torch.cuda.synchronize()
+            _lib.check(ctx.lib.fp_op_gemm(ctx.h, epi, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                          M, N, K))
+            ctx.sync()
+            outs.append(out)
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+    assert torch.equal(outs[0], outs[1])
+    err = (outs[0].float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    tol = 1e-5 * scale * K ** 0.5 if epi == 1 else 2 ** -7 * scale + 1e-3
+    assert err <= tol, (err, scale)
+
+
+@pytest.mark.parametrize("policy", [-1, 3])
 @pytest.mark.parametrize("M,F,K", [(1, 128, 64), (300, 512, 512), (4096, 1536, 512),
-                                   (77, 14336 // 4, 4096)])
-def test_gate_up_swiglu(ctx, M, F, K):
+                                   (77, 14336 // 4, 4096), (386, 14336, 4096)])
+def test_gate_up_swiglu(ctx, M, F, K, policy):
     """gate_up GEMM + SwiGLU epilogue vs torch fp32: silu(x Wg^T) * (x Wu^T)."""
     import torch
 
@@ -139,9 +180,13 @@ def test_gate_up_swiglu(ctx, M, F, K):
     wu = torch.randn(F, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
     out = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
     torch.cuda.synchronize()
-    _lib.check(ctx.lib.fp_op_gate_up_swiglu(ctx.h, x.data_ptr(), wg.data_ptr(), wu.data_ptr(),
-                                            out.data_ptr(), M, F, K))
-    ctx.sync()
+    try:
+        _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, policy, 0))
+        _lib.check(ctx.lib.fp_op_gate_up_swiglu(ctx.h, x.data_ptr(), wg.data_ptr(), wu.data_ptr(),
+                                                out.data_ptr(), M, F, K))
+        ctx.sync()
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
     xf = x.float()
     ref = torch.nn.functional.silu(xf @ wg.float().t()) * (xf @ wu.float().t())
     err = (out.float() - ref).abs().max().item()
