@@ -233,6 +233,14 @@ int fp_tp_enqueue_lockstep(fp_ctx** ctxs, fp_task** tasks, int32_t n, int32_t fi
 /* Synchronises and reads the rank's device counters: [exchanges, boundaries decided,
  * gemm ticket, all-reduce ticket] (tickets are 0 between kernels). */
 int fp_ctx_tp_counters(fp_ctx* ctx, int32_t* out4);
+/* The row-parallel exchange as a per-op entry point: for every rank i driven by this caller
+ * (all ranks of a lock-step group, or this process's rank of a multi-process group),
+ * h_i[M, hidden] = bf16(h_i + part_0 + ... + part_{tp-1}) (fp32 sum in rank order; the
+ * partials of ranks not in `ctxs` come from their own callers). Device pointers; M <= the
+ * exchange capacity. The reference models this step only as `/tp * (1 + tp_comm_overhead)`
+ * (prefillsim/cost_model.py:99-100,166). */
+int fp_op_tp_allreduce(fp_ctx** ctxs, int32_t n, void* const* h, const void* const* parts,
+                       int32_t M);
 
 /* ---- per-operator entry points (device pointers; unit tests and microbenchmarks) -------- */
 /* C[M,N] = A[M,K] B[N,K]^T; epi: 0 bf16 store, 1 fp32 store, 2 residual add into C (bf16). */
@@ -243,6 +251,16 @@ int fp_op_rmsnorm(fp_ctx* ctx, const void* x, const void* gamma, void* out, int3
 /* out[M, F] = silu(x W_gate^T) * (x W_up^T): the gate_up_proj GEMM with its SwiGLU epilogue. */
 int fp_op_gate_up_swiglu(fp_ctx* ctx, const void* x, const void* w_gate, const void* w_up,
                          void* out, int32_t M, int32_t F, int32_t K);
+/* qkv_proj with its fused epilogue (fp_task's entry 0 of a layer minus the input norm):
+ * [q | k | v] = x W_qkv^T (W_qkv [q_cols + 2 kv_cols, K], q heads, then k heads, then v heads,
+ * 128 columns each), RoPE (rotate-half, the context's rope_theta, positions[m] < max_pos) on q
+ * and k, q -> q_out [M, q_cols], k and v -> the paged layout kv_pages[page][k|v][kv head]
+ * [positions[m] % page_size][128] of the page tok_page[m] (the forward pass's KV write). All
+ * pointers are device memory. Replaces the reference's per-kind cost of `qkv_proj`
+ * (prefillsim/cost_model.py:151-166) with the computation. */
+int fp_op_qkv_rope_kv(fp_ctx* ctx, const void* x, const void* w_qkv, void* q_out, void* kv_pages,
+                      const int32_t* positions, const int32_t* tok_page, int32_t M, int32_t q_cols,
+                      int32_t kv_cols, int32_t K);
 /* Causal prefill attention of one request's last n_q tokens over kv_len keys (prefix =
  * kv_len - n_q): q/out [n_q, n_heads*128], k/v [kv_len, n_kv_heads*128] (bf16, device); K/V go
  * through the paged pool like the forward pass (borrowed free pages). */

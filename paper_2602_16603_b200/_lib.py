@@ -125,6 +125,8 @@ _SIGS = {
     "fp_ctx_set_gemm_policy": (C.c_int, [_P, _I, _I]),
     "fp_task_read_routing": (C.c_int, [_P, _P, _P, _P, _I]),
     "fp_op_gate_up_swiglu": (C.c_int, [_P, _P, _P, _P, _P, _I, _I, _I]),
+    "fp_op_qkv_rope_kv": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I]),
+    "fp_op_tp_allreduce": (C.c_int, [_P, _I, _P, _P, _I]),
     "fp_op_attn_prefill": (C.c_int, [_P, _P, _P, _P, _P, _I, _I]),
     "fp_debug_gemm_stamps": (C.c_int, [_P, _P, _I]),
     "fp_sync": (C.c_int, [_P]),

@@ -489,10 +489,12 @@ static SkPlan plan_streamk(const fp_ctx* c, int M, int N, int K) {
   SkPlan pl;
   const int T = ((M + kGemmBM - 1) / kGemmBM) * (N / 256), nk = K / kGemmBK, G0 = c->num_sms;
   const int waves = T / G0;
-  if (waves < 1 && c->force_pair != 3) return pl;  // at most one partner per tile
   pl.dp_tiles = waves >= 2 ? (waves - 1) * G0 : 0;
   const long long U = (long long)(T - pl.dp_tiles) * nk;
   pl.grid = (int)std::min<long long>(G0, U / kSkMinKb);
+  // an under-filled launch gets at most two CTAs per tile (one partner each): a partner costs
+  // far more than the k-blocks a third CTA would save
+  if (waves < 1 && c->force_pair != 3) pl.grid = std::min(pl.grid, 2 * T);
   if (pl.grid < 2) return pl;
   const double per = std::ceil((double)U / pl.grid);
   const double partners = std::ceil(nk / per);
@@ -1966,6 +1968,47 @@ int fp_op_gate_up_swiglu(fp_ctx* c, const void* x, const void* w_gate, const voi
   return FP_OK;
 }
 
+int fp_op_qkv_rope_kv(fp_ctx* c, const void* x, const void* w_qkv, void* q_out, void* kv_pages,
+                      const int32_t* positions, const int32_t* tok_page, int32_t M, int32_t q_cols,
+                      int32_t kv_cols, int32_t K) {
+  REQ(c && x && w_qkv && q_out && kv_pages && positions && tok_page, "null argument");
+  REQ(M >= 1 && K % 64 == 0 && q_cols % 128 == 0 && kv_cols % 128 == 0 && kv_cols > 0,
+      "qkv op: K%64, q_cols%128 and kv_cols%128 required");
+  CK(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lk(c->launch_mu);
+  // weight rows padded to a multiple of 256 with zeros (the model's qkv layout)
+  const int n = q_cols + 2 * kv_cols, N = (n + 255) / 256 * 256;
+  __nv_bfloat16* w = nullptr;
+  CK(cudaMallocAsync((void**)&w, (size_t)N * K * 2, c->stream));
+  CK(cudaMemsetAsync(w, 0, (size_t)N * K * 2, c->stream));
+  CK(cudaMemcpyAsync(w, w_qkv, (size_t)n * K * 2, cudaMemcpyDeviceToDevice, c->stream));
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_map(&ta, x, M, K, 128)) || (rc = make_map(&tb, w, N, K, 128))) {
+    cudaFreeAsync(w, c->stream);
+    return rc;
+  }
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.pos = positions;
+  p.tok_page = tok_page;
+  p.qbuf = static_cast<__nv_bfloat16*>(q_out);
+  p.ldq = q_cols;
+  p.kv_layer = static_cast<__nv_bfloat16*>(kv_pages);
+  p.rope = c->rope;
+  p.q_cols = q_cols;
+  p.kv_cols = kv_cols;
+  p.page_size = c->page_size;
+  p.n_kv_heads = kv_cols / 128;
+  p.norm_eps = c->cfg.rms_eps;
+  launch_gemm<EPI_QKV>(c, ta, tb, p, c->stream);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(w, c->stream));
+  return FP_OK;
+}
+
 int fp_op_attn_prefill(fp_ctx* c, const void* q, const void* k, const void* v, void* out,
                        int32_t n_q, int32_t kv_len) {
   REQ(c && q && k && v && out, "null argument");
@@ -2174,6 +2217,45 @@ int fp_tp_connect_local(fp_ctx** ctxs, int32_t n, int64_t max_tokens) {
       ctxs[r]->tp_lockstep = true;
     }
   }
+  return FP_OK;
+}
+
+int fp_op_tp_allreduce(fp_ctx** ctxs, int32_t n, void* const* h, const void* const* parts,
+                       int32_t M) {
+  REQ(ctxs && h && parts && n >= 1 && M >= 1, "null argument");
+  for (int i = 0; i < n; ++i) {
+    REQ(ctxs[i] && ctxs[i]->tp_connected && ctxs[i]->d_tp, "context is not a connected TP rank");
+    REQ(M <= ctxs[i]->tp_host.part_rows, "M exceeds the exchange capacity");
+    REQ(h[i] && parts[i], "null buffer");
+  }
+  CK(cudaSetDevice(ctxs[0]->device));
+  const int d = ctxs[0]->cfg.hidden;
+  const long long vecs = (long long)M * d / 8;
+  const int grid = (int)std::max(1LL, std::min<long long>((vecs + 255) / 256, 4LL * ctxs[0]->num_sms));
+  std::vector<float*> ssq(n, nullptr);
+  // every caller-driven rank publishes before any of them waits (lock-step ranks share a stream)
+  for (int i = 0; i < n; ++i) {
+    fp_ctx* c = ctxs[i];
+    std::lock_guard<std::mutex> lk(c->launch_mu);
+    CK(cudaMallocAsync((void**)&ssq[i], (size_t)M * (d / 128) * 4, c->stream));
+    tp_stage_partial_kernel<<<grid, 256, 0, c->stream>>>(
+        c->d_tp, static_cast<const __nv_bfloat16*>(parts[i]), vecs);
+  }
+  for (int i = 0; i < n; ++i) {
+    fp_ctx* c = ctxs[i];
+    std::lock_guard<std::mutex> lk(c->launch_mu);
+    XchgParams x{};
+    x.M = M;
+    x.d = d;
+    x.h = static_cast<__nv_bfloat16*>(h[i]);
+    x.ldh = d;
+    x.ssq = ssq[i];
+    x.guard.tp = c->d_tp;  // unguarded (no task): the boundary check passes
+    const int g2 = (int)std::max(1LL, std::min<long long>((vecs + 255) / 256, 8LL * c->num_sms));
+    tp_allreduce_kernel<<<g2, 256, 0, c->stream>>>(x);
+    CK(cudaFreeAsync(ssq[i], c->stream));
+  }
+  CK(cudaGetLastError());
   return FP_OK;
 }
 

@@ -110,4 +110,20 @@ __global__ void __launch_bounds__(256) tp_allreduce_kernel(const XchgParams p) {
   }
 }
 
+// Per-op all-reduce (fp_op_tp_allreduce): stage a caller partial into this rank's exchange
+// slot and publish it exactly like an exchange GEMM's epilogue does (tp_publish_partial).
+__global__ void __launch_bounds__(256) tp_stage_partial_kernel(const TpDev* tp,
+                                                               const __nv_bfloat16* src,
+                                                               long long vecs) {
+  grid_dep_wait();
+  const int xc = *(volatile int*)&tp->local->xcount;
+  uint4* dst = reinterpret_cast<uint4*>(tp->part[tp->rank][xc & 1]);
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < vecs;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = ld_nc_v4(s + i);
+  __syncthreads();
+  if (threadIdx.x == 0) tp_publish_partial(tp);
+}
+
 }  // namespace fp

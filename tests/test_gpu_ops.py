@@ -193,6 +193,57 @@ def test_gate_up_swiglu(ctx, M, F, K, policy):
     assert err <= 2 ** -7 * ref.abs().max().item() + 1e-3, err
 
 
+@pytest.mark.parametrize("M,q_cols,kv_cols,K", [(1, 512, 256, 512), (77, 512, 256, 512),
+                                                 (300, 4096, 1024, 1024), (700, 1024, 128, 256)])
+def test_qkv_rope_kv(ctx, M, q_cols, kv_cols, K):
+    """qkv_proj with its fused epilogue vs torch fp32: [q|k|v] = x W^T, rotate-half RoPE on q and
+    k at arbitrary positions (the context's theta), K/V scattered into the paged layout."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+
+    ps, theta, n_pages = 128, ctx.shape.rope_theta, 8
+    hkv = kv_cols // 128
+    g = torch.Generator(device="cuda").manual_seed(M + q_cols + K)
+    x = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    w = torch.randn(q_cols + 2 * kv_cols, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    pos = torch.randperm(n_pages * ps, generator=torch.Generator().manual_seed(M))[:M]
+    page_of = torch.randperm(n_pages, generator=torch.Generator().manual_seed(K))
+    tok_page = page_of[pos // ps]
+    pos_d = pos.to(torch.int32).cuda()
+    tp_d = tok_page.to(torch.int32).cuda()
+    q = torch.empty(M, q_cols, device="cuda", dtype=torch.bfloat16)
+    kv = torch.zeros(n_pages, 2, hkv, ps, 128, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    _lib.check(ctx.lib.fp_op_qkv_rope_kv(ctx.h, x.data_ptr(), w.data_ptr(), q.data_ptr(),
+                                         kv.data_ptr(), pos_d.data_ptr(), tp_d.data_ptr(), M,
+                                         q_cols, kv_cols, K))
+    ctx.sync()
+    y = x.float() @ w.float().t()
+    inv = theta ** (-torch.arange(64, dtype=torch.float64) * 2 / 128)
+    ang = pos.double()[:, None] * inv[None, :]
+    cos, sin = ang.cos().float().cuda(), ang.sin().float().cuda()
+
+    def rope(t):  # [M, heads*128], rotate-half per head
+        t = t.view(M, -1, 128)
+        a, b = t[..., :64], t[..., 64:]
+        return torch.cat([a * cos[:, None] - b * sin[:, None], b * cos[:, None] + a * sin[:, None]],
+                         -1).view(M, -1)
+
+    q_ref = rope(y[:, :q_cols])
+    k_ref = rope(y[:, q_cols:q_cols + kv_cols]).view(M, hkv, 128)
+    v_ref = y[:, q_cols + kv_cols:].view(M, hkv, 128)
+    k_got = kv[tok_page.cuda(), 0, :, (pos % ps).cuda()].float()
+    v_got = kv[tok_page.cuda(), 1, :, (pos % ps).cuda()].float()
+    for got, ref in ((q.float(), q_ref), (k_got, k_ref), (v_got, v_ref)):
+        err = (got - ref).abs().max().item()
+        assert err <= 2 ** -7 * ref.abs().max().item() + 1e-3, err
+    written = torch.zeros(n_pages, ps, dtype=torch.bool)
+    written[tok_page, pos % ps] = True
+    untouched = kv.permute(0, 3, 1, 2, 4)[~written.cuda()]
+    assert untouched.abs().max().item() == 0  # nothing outside the tokens' slots
+
+
 @pytest.mark.parametrize("n_q,kv_len", [(1, 1), (37, 37), (128, 128), (200, 200), (130, 700),
                                         (1000, 1000), (64, 4096), (513, 2049)])
 def test_attn_prefill_vs_torch(n_q, kv_len):

@@ -228,3 +228,41 @@ def test_qwen25_32b_shape_tp_reference_parity(tp):
     for rid in (0, 1):
         assert np.isfinite(b.logits[rid]).all() and np.abs(b.logits[rid]).max() > 0
     g.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_op_tp_allreduce(tp):
+    """fp_op_tp_allreduce (the row-parallel exchange as a per-op entry point): every rank's h
+    becomes bf16(h + part_0 + ... + part_{tp-1}) with the fp32 sum in rank order -- bit-exact
+    against torch, identical on every rank, over consecutive exchanges (both slots)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import TPGroup
+
+    shape = SHAPES[NAME]
+    g = TPGroup(shape, tp, kv_pages=8, max_pos=1024, max_tokens=512)
+    try:
+        ctxs = (C.c_void_p * tp)(*[c.h.value for c in g.ranks])
+        gen = torch.Generator(device="cuda").manual_seed(tp)
+        for M in (300, 1, 512):
+            h0 = torch.randn(M, shape.hidden, device="cuda", generator=gen).to(torch.bfloat16)
+            hs = [h0.clone() for _ in range(tp)]
+            parts = [torch.randn(M, shape.hidden, device="cuda", generator=gen).to(torch.bfloat16)
+                     for _ in range(tp)]
+            torch.cuda.synchronize()
+            hp = (C.c_void_p * tp)(*[x.data_ptr() for x in hs])
+            pp = (C.c_void_p * tp)(*[x.data_ptr() for x in parts])
+            _lib.check(g.lib.fp_op_tp_allreduce(ctxs, tp, hp, pp, M), "fp_op_tp_allreduce")
+            g.sync()
+            acc = h0.float()
+            for p in parts:
+                acc = acc + p.float()
+            ref = acc.to(torch.bfloat16)
+            for r in range(tp):
+                assert torch.equal(hs[r], ref), r
+    finally:
+        g.close()
