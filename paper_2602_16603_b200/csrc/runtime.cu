@@ -670,7 +670,7 @@ static int launch_moe_entry(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, 
   if (op == FP_OP_GATE) {
     GemmParams p{};
     p.M = M;
-    p.N = 256;
+    p.N = E <= 128 ? 128 : 256;  // router rows are padded to 256; compute only what is real
     p.K = d;
     p.out = t->rlog;
     p.ldo = 256;
@@ -680,7 +680,8 @@ static int launch_moe_entry(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, 
     p.guard = g;
     {
       ProfScope ps(c, st, FP_K_ROUTER, layer, M, 2.0 * M * E * d, 0.0);
-      launch_gemm<EPI_STORE_F32>(c, t->tm_h, ly.tm_r, p, st);
+      if (p.N == 128) launch_gemm_cg<EPI_STORE_F32, 1, 128>(c, t->tm_h, ly.tm_r, p, st);
+      else launch_gemm<EPI_STORE_F32>(c, t->tm_h, ly.tm_r, p, st);
     }
     ProfScope ps(c, st, FP_K_MOE_DISPATCH, layer, M, 0.0, rows * d * 2 * 2);
     launch_pdl(moe_route_kernel, dim3(tok_blocks), dim3(256), 0, st, mp);
