@@ -228,10 +228,11 @@ struct fp_ctx {
   bool use_narrow = true;  // FP_NARROW=0: never 128 x 128 tiles (experiments)
   int force_splits = 0;   // FP_FORCE_SPLITS (experiments)
   int force_pair = -1;    // FP_FORCE_PAIR (experiments): 0 single, 1 pair, 2 narrow, 3 stream-K
-  // FP_STREAMK=1: stream-K where its cost model wins. Off by default: measured neutral on the
-  // power-capped B200 (the idle SMs of a partial wave cost little energy; the partial
-  // round trips add traffic), forced by policy 3 in the parity tests.
-  bool use_streamk = false;
+  // Stream-K where plan_streamk allows it (under-filled long-K launches) and its cost model
+  // wins; FP_STREAMK=0 disables. Everywhere else it measured neutral or worse on the
+  // power-capped B200 (the idle SMs of a partial wave cost little energy; the partial round
+  // trips add traffic). Policy 3 forces it in the parity tests.
+  bool use_streamk = true;
   int* sk_flags = nullptr;  // stream-K partial flags [num_sms]
   int sk_epoch = 0;         // per stream-K launch (flags compare against it: no reset)
 };
@@ -489,6 +490,9 @@ static SkPlan plan_streamk(const fp_ctx* c, int M, int N, int K) {
   SkPlan pl;
   const int T = ((M + kGemmBM - 1) / kGemmBM) * (N / 256), nk = K / kGemmBK, G0 = c->num_sms;
   const int waves = T / G0;
+  // automatic use only where it measured a win: under-filled long-K launches (down_proj of
+  // mid-size requests, -18% at M = 545); elsewhere pair tiles win (tools/gemm_probe.py)
+  if (c->force_pair != 3 && (waves >= 1 || nk < 128)) return pl;
   pl.dp_tiles = waves >= 2 ? (waves - 1) * G0 : 0;
   const long long U = (long long)(T - pl.dp_tiles) * nk;
   pl.grid = (int)std::min<long long>(G0, U / kSkMinKb);
