@@ -49,7 +49,10 @@ def entry_samples(records: Sequence[dict]) -> dict:
 
 
 def fit_cost_params(records: Sequence[dict], num_layers: int, c_check: float = 1e-6):
-    """Least-squares CostParams from profile records (single-request tasks: quad = M^2)."""
+    """CostParams from profile records (single-request tasks: quad = M^2), least squares on the
+    RELATIVE error: the profile spans 40-token to 5K-token entries, and an absolute fit would
+    let the long entries set every coefficient (max relative error 39% on the short ones),
+    while the scheduler's slack and batching decisions need short requests predicted too."""
     ps = refsim.load()
     OK = ps.OperatorKind
     samples = entry_samples(records)
@@ -65,7 +68,8 @@ def fit_cost_params(records: Sequence[dict], num_layers: int, c_check: float = 1
             X = np.stack([np.ones_like(m), m, m * m], axis=1)
         else:
             X = np.stack([np.ones_like(m), m], axis=1)
-        coef, *_ = np.linalg.lstsq(X, y, rcond=None)
+        wgt = 1.0 / np.maximum(y, 1e-9)
+        coef, *_ = np.linalg.lstsq(X * wgt[:, None], y * wgt, rcond=None)
         coef = np.maximum(coef, 0.0)  # the reference rejects negative coefficients
         c_fix[OK(op)] = float(coef[0])
         c_lin[OK(op)] = float(coef[1])
