@@ -15,8 +15,10 @@ def short(name):
     epi = {"0": "store_bf16", "1": "store_f32(lm_head)", "2": "resid(o/down)", "3": "swiglu(gate_up)", "4": "qkv_rope_kv"}
     m = re.search(r"gemm_bf16_tn_kernel<(?:\(int\))?(\d+), *(?:\(int\))?(\d+), *(?:\(int\))?(\d+)(?:, *(?:\(bool\))?(\w+))?>", name)
     if m:
-        split = " split-capable" if m.group(4) in ("1", "true") else ""
-        return f"gemm {epi.get(m.group(2), m.group(2))} cta_group={m.group(3)}{split}"
+        mode = {"1": " split-capable", "true": " split-capable", "2": " grouped(MoE)",
+                "3": " stream-K"}.get(m.group(4), "")
+        width = "" if m.group(1) == "256" else f" {m.group(1)}-wide"
+        return f"gemm {epi.get(m.group(2), m.group(2))} cta_group={m.group(3)}{width}{mode}"
     for k in ("attn_prefill_tc_kernel", "rmsnorm_kernel", "init_normal_kernel"):
         if k in name:
             return k
