@@ -21,7 +21,8 @@ Reported (one JSON line from rank 0):
   p99_preempt  host-observed signal -> device ACK latency on a long request, async launch
                worker, vs the longest operator of that request.
   goodput      req/s at 90% TTFT-SLO attainment from the reference goodput_search with the
-               cost model re-fitted to this run's B200 kernel timings (virtual clock).
+               cost model re-fitted to this run's B200 kernel timings (virtual clock), and a
+               live wall-clock replay of the config-2 arrivals on the GPU (live_check).
   cpu_baseline the fp32 numpy restatement (oracle/) on this host's cores, bounded sample.
 """
 
