@@ -116,34 +116,44 @@ __global__ void __launch_bounds__(256) moe_route_kernel(const MoeParams p) {
 }
 
 // One CTA: expert offsets (exclusive scan of the histogram) and the grouped GEMMs' m-tile
-// table; re-arms the histogram and the scatter cursors.
+// table; re-arms the histogram and the scatter cursors. Block-wide scan: warp shuffles, then
+// the 8 warp totals.
 __global__ void __launch_bounds__(kMoeMaxExperts) moe_plan_kernel(const MoeParams p) {
-  __shared__ int s_cnt[kMoeMaxExperts], s_off[kMoeMaxExperts + 1], s_tiles[kMoeMaxExperts + 1];
+  __shared__ int s_wa[kMoeMaxExperts / 32], s_wb[kMoeMaxExperts / 32];
   grid_dep_wait();
   if (!guard_block(p.guard)) return;
-  const int e = threadIdx.x;
+  const int e = threadIdx.x, lane = e & 31, warp = e >> 5;
   const int cnt = e < p.n_experts ? p.counts[e] : 0;
-  s_cnt[e] = cnt;
-  __syncthreads();
-  if (e == 0) {
-    int o = 0, t = 0;
-    for (int i = 0; i < p.n_experts; ++i) {
-      s_off[i] = o;
-      s_tiles[i] = t;
-      o += s_cnt[i];
-      t += (s_cnt[i] + 127) / 128;
+  const int nt = (cnt + 127) / 128;
+  int a = cnt, b = nt;  // inclusive scans of rows and m-tiles
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
+    if (lane >= o) {
+      a += x;
+      b += y;
     }
-    s_off[p.n_experts] = o;
-    s_tiles[p.n_experts] = t;
-    *p.mtile_count = t;
+  }
+  if (lane == 31) {
+    s_wa[warp] = a;
+    s_wb[warp] = b;
   }
   __syncthreads();
-  if (e < p.n_experts) p.offsets[e] = s_off[e];
-  if (e == 0) p.offsets[p.n_experts] = s_off[p.n_experts];
+  int pa = 0, pb = 0;  // totals of the warps before this one
+  for (int w = 0; w < warp; ++w) {
+    pa += s_wa[w];
+    pb += s_wb[w];
+  }
+  const int off = pa + a - cnt, t0 = pb + b - nt;
   if (e < p.n_experts) {
-    for (int k = 0; k < (cnt + 127) / 128; ++k) p.mtiles[s_tiles[e] + k] = make_int2(e, s_off[e] + 128 * k);
+    p.offsets[e] = off;
+    for (int k = 0; k < nt; ++k) p.mtiles[t0 + k] = make_int2(e, off + 128 * k);
     p.counts[e] = 0;
     p.cursor[e] = 0;
+  }
+  if (e == kMoeMaxExperts - 1) {  // the last thread's inclusive sums are the totals
+    p.offsets[p.n_experts] = pa + a;
+    *p.mtile_count = pb + b;
   }
 }
 
