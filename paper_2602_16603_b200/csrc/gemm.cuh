@@ -453,7 +453,7 @@ __device__ __noinline__ void split_item_epilogue(const GemmParams& p, const Gmem
 // MODE 0: plain tiles. MODE 1: the instantiation that also runs tail split-K tiles (launched only
 // when the launcher chose splits > 1; MODE 0 carries no split code and no extra registers).
 // MODE 2: grouped GEMM for MoE experts -- A rows are expert-ordered segments, the m-tile table
-// (expert, first row) and its length come from device memory (moe_plan_kernel), the B rows of
+// (expert, first row) and its length come from device memory (moe_plan_block), the B rows of
 // expert e start at e * grp_b_rows, rows past the expert's segment are masked, and the fused
 // norm looks up each row's token through grp_perm. CG = 1 only.
 template <int BN, int EPI, int CG, int MODE>

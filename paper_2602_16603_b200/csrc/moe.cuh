@@ -8,9 +8,9 @@
 // output is sum_j w_j * expert_{e_j}(x).
 //
 // gate entry:    router GEMM (tcgen05, fused post-attention norm, fp32 logits)
-//                -> moe_route_kernel   softmax / top-k per token, expert histogram
-//                -> moe_plan_kernel    expert row offsets (exclusive scan) + the m-tile table of
-//                                      the grouped GEMMs
+//                -> moe_route_kernel   softmax / top-k per token, expert histogram; its last
+//                                      block plans: expert row offsets (exclusive scan) + the
+//                                      m-tile table of the grouped GEMMs
 //                -> moe_scatter_kernel token rows gathered into expert-contiguous order
 // experts entry: grouped gate/up + SwiGLU GEMM -> grouped down GEMM (gemm.cuh MODE 2)
 //                -> moe_combine_kernel h += sum_j w_j y_j (j order: deterministic), and the
@@ -41,6 +41,7 @@ struct MoeParams {
   int* mtile_count;      // number of 128-row m-tiles of the grouped GEMMs
   int2* mtiles;          // [max_mtiles] (expert, first row)
   int* perm_tok;         // [M * top_k] token of each expert-ordered row
+  int* ticket;           // route blocks finished (the last one plans; zero between gate entries)
   const __nv_bfloat16* h;  // residual stream [M, d] (scatter source, combine target)
   __nv_bfloat16* h_out;
   __nv_bfloat16* xperm;  // [M * top_k, d] gathered rows
@@ -49,13 +50,7 @@ struct MoeParams {
   Guard guard;
 };
 
-// One warp per token: softmax over the experts, top-k by repeated warp argmax.
-__global__ void __launch_bounds__(256) moe_route_kernel(const MoeParams p) {
-  grid_dep_wait();
-  if (!guard_block(p.guard)) return;
-  const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (t >= p.M) return;
+DEVI void moe_route_token(const MoeParams& p, int t, int lane) {
   constexpr int PER = kMoeMaxExperts / 32;
   float v[PER];
   const float* lg = p.logits + (long long)t * p.ld_logits;
@@ -115,15 +110,13 @@ __global__ void __launch_bounds__(256) moe_route_kernel(const MoeParams p) {
   }
 }
 
-// One CTA: expert offsets (exclusive scan of the histogram) and the grouped GEMMs' m-tile
-// table; re-arms the histogram and the scatter cursors. Block-wide scan: warp shuffles, then
-// the 8 warp totals.
-__global__ void __launch_bounds__(kMoeMaxExperts) moe_plan_kernel(const MoeParams p) {
+// The plan, by one block of kMoeMaxExperts threads: expert offsets (exclusive scan of the
+// histogram) and the grouped GEMMs' m-tile table; re-arms the histogram and the scatter cursors.
+// Block-wide scan: warp shuffles, then the warp totals.
+DEVI void moe_plan_block(const MoeParams& p) {
   __shared__ int s_wa[kMoeMaxExperts / 32], s_wb[kMoeMaxExperts / 32];
-  grid_dep_wait();
-  if (!guard_block(p.guard)) return;
   const int e = threadIdx.x, lane = e & 31, warp = e >> 5;
-  const int cnt = e < p.n_experts ? p.counts[e] : 0;
+  const int cnt = e < p.n_experts ? __ldcg(p.counts + e) : 0;
   const int nt = (cnt + 127) / 128;
   int a = cnt, b = nt;  // inclusive scans of rows and m-tiles
 #pragma unroll
@@ -155,6 +148,28 @@ __global__ void __launch_bounds__(kMoeMaxExperts) moe_plan_kernel(const MoeParam
     p.offsets[p.n_experts] = pa + a;
     *p.mtile_count = pb + b;
   }
+}
+
+// One warp per token: softmax over the experts, top-k by repeated warp argmax, expert histogram;
+// the last block to finish turns the histogram into the plan (moe_plan_block).
+__global__ void __launch_bounds__(256) moe_route_kernel(const MoeParams p) {
+  grid_dep_wait();
+  if (!guard_block(p.guard)) return;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t < p.M) moe_route_token(p, t, lane);
+  __shared__ int s_last;
+  __threadfence();  // this thread's histogram atomics are ordered before the ticket
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(p.ticket, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();  // every block's histogram is visible
+  moe_plan_block(p);
+  if (threadIdx.x == 0) *p.ticket = 0;
 }
 
 // One warp per token: claim a row in each chosen expert's segment and copy the token's h row.

@@ -663,6 +663,7 @@ static int launch_moe_entry(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, 
   mp.mtile_count = t->m_mtc;
   mp.mtiles = t->m_mtiles;
   mp.perm_tok = t->m_perm;
+  mp.ticket = t->m_perm + (long long)t->max_m * K;  // the first slack int after perm (zeroed)
   mp.h = t->h;
   mp.h_out = t->h;
   mp.xperm = t->xperm;
@@ -688,8 +689,7 @@ static int launch_moe_entry(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, 
       else launch_gemm<EPI_STORE_F32>(c, t->tm_h, ly.tm_r, p, st);
     }
     ProfScope ps(c, st, FP_K_MOE_DISPATCH, layer, M, 0.0, rows * d * 2 * 2);
-    launch_pdl(moe_route_kernel, dim3(tok_blocks), dim3(256), 0, st, mp);
-    launch_pdl(moe_plan_kernel, dim3(1), dim3(kMoeMaxExperts), 0, st, mp);
+    launch_pdl(moe_route_kernel, dim3(tok_blocks), dim3(256), 0, st, mp);  // + plan (last block)
     launch_pdl(moe_scatter_kernel, dim3(tok_blocks), dim3(256), 0, st, mp);
     t->moe_rows = M;
     return FP_OK;
