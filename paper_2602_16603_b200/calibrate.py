@@ -48,6 +48,15 @@ def entry_samples(records: Sequence[dict]) -> dict:
     return out
 
 
+def _medians(pts):
+    """One point per entry size: the median duration over its launches (a profile holds every
+    layer of every request, so one clock dip or preempted neighbour does not steer the fit)."""
+    by = defaultdict(list)
+    for m, y in pts:
+        by[m].append(y)
+    return [(m, float(np.median(v))) for m, v in sorted(by.items())]
+
+
 def fit_cost_params(records: Sequence[dict], num_layers: int, c_check: float = 1e-6):
     """CostParams from profile records (single-request tasks: quad = M^2), least squares on the
     RELATIVE error: the profile spans 40-token to 5K-token entries, and an absolute fit would
@@ -59,7 +68,7 @@ def fit_cost_params(records: Sequence[dict], num_layers: int, c_check: float = 1
     c_lin, c_fix = {}, {}
     c_attn = 0.0
     for op in ("qkv_proj", "attn", "o_proj", "gate_up_proj", "down_proj"):
-        pts = samples.get(op, [])
+        pts = _medians(samples.get(op, []))
         if not pts:
             raise ValueError(f"no samples for {op}")
         m = np.array([p[0] for p in pts], dtype=np.float64)
@@ -82,13 +91,14 @@ def fit_cost_params(records: Sequence[dict], num_layers: int, c_check: float = 1
 
 
 def predicted_vs_measured(params, records: Sequence[dict]) -> float:
-    """Max relative error of the fitted per-entry model over the profiled entries."""
+    """Max relative error of the fitted per-entry model over the profiled entry sizes (median
+    duration per size)."""
     ps = refsim.load()
     worst = 0.0
     for op, pts in entry_samples(records).items():
         if op.startswith("_"):
             continue
-        for m, y in pts:
+        for m, y in _medians(pts):
             pred = ps.operator_duration(ps.OperatorKind(op), int(m), 0, params)
             worst = max(worst, abs(pred - y) / max(y, 1e-9))
     return worst
