@@ -1411,15 +1411,18 @@ int fp_weights_init_random(fp_ctx* c, uint64_t seed, float stdv) {
   return FP_OK;
 }
 
-int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n_seqs,
-                   int32_t chunk_tokens, int32_t granularity, int32_t task_id, fp_task** out) {
-  REQ(c && ids && lens && out, "null argument");
+// Builds the task into *tp (set as soon as it exists, so the caller can release a partially
+// built task when an allocation fails); validation failures delete it and leave *tp null.
+static int task_create_impl(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n_seqs,
+                            int32_t chunk_tokens, int32_t granularity, int32_t task_id, Task** tp) {
+  REQ(c && ids && lens, "null argument");
   REQ(n_seqs >= 1, "per_request_tokens must be non-empty");  // cost_model.py:205-206
   REQ(chunk_tokens >= 0, "chunk_tokens must be >= 0");
   REQ(granularity >= 0 && granularity <= 3, "bad granularity");
   const fp_model_cfg& m = c->cfg;
   CK(cudaSetDevice(c->device));
   Task* t = new Task();
+  *tp = t;
   t->id = task_id;
   t->n_seqs = n_seqs;
   t->L = m.num_layers;
@@ -1429,10 +1432,12 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   for (int i = 0; i < n_seqs; ++i) {
     if (lens[i] < 1) {
       delete t;
+      *tp = nullptr;
       return set_err(FP_ERR_ARG, "all token counts must be >= 1");  // cost_model.py:207-208
     }
     if (lens[i] > m.max_pos) {
       delete t;
+      *tp = nullptr;
       return set_err(FP_ERR_ARG, "request longer than max_pos");
     }
     total += lens[i];
@@ -1446,12 +1451,14 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
                           : nullptr;
     if (why) {
       delete t;
+      *tp = nullptr;
       return set_err(FP_ERR_STATE, why);
     }
   }
   for (long long i = 0; i < total; ++i)
     if (ids[i] < 0 || ids[i] >= m.vocab) {
       delete t;
+      *tp = nullptr;
       return set_err(FP_ERR_ARG, "token id out of range");
     }
   // pages
@@ -1467,6 +1474,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
     std::lock_guard<std::mutex> lk(c->page_mu);
     if ((int)c->free_pages.size() < need) {
       delete t;
+      *tp = nullptr;
       return set_err(FP_ERR_NOMEM, "KV page pool exhausted");
     }
     for (int i = 0; i < need; ++i) {
@@ -1635,6 +1643,36 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&t->fence, cudaEventDisableTiming));
   CK(cudaEventRecord(t->fence, up));
+  return FP_OK;
+}
+
+// A task whose creation failed part-way: nothing of it was launched; drain its uploads, free
+// what was allocated and return its KV pages (no leak when the device runs out of memory).
+static void task_release_partial(fp_ctx* c, Task* t) {
+  cudaStreamSynchronize(c->upload);
+  void* bufs[] = {t->meta, t->h, t->ssq, t->q, t->ao, t->act, t->rlog, t->moe_meta,
+                  t->xperm, t->actp, t->yperm, t->xf, t->logits, t->ctl};
+  for (void* b : bufs)
+    if (b) cudaFreeAsync(b, c->upload);
+  cudaStreamSynchronize(c->upload);
+  for (cudaEvent_t e : {t->ready, t->done, t->fence})
+    if (e) cudaEventDestroy(e);
+  {
+    std::lock_guard<std::mutex> lk(c->page_mu);
+    for (int p : t->pages) c->free_pages.push_back(p);
+  }
+  delete t;
+}
+
+int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n_seqs,
+                   int32_t chunk_tokens, int32_t granularity, int32_t task_id, fp_task** out) {
+  REQ(out, "null argument");
+  Task* t = nullptr;
+  const int rc = task_create_impl(c, ids, lens, n_seqs, chunk_tokens, granularity, task_id, &t);
+  if (rc != FP_OK) {
+    if (t) task_release_partial(c, t);
+    return rc;
+  }
   *out = reinterpret_cast<fp_task*>(t);
   return FP_OK;
 }

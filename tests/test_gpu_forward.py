@@ -189,3 +189,27 @@ def test_forced_gemm_tiling_vs_oracle(tiny, policy):
     for r, (k, v) in enumerate(kv):
         assert rel_err(k, ot.k_cache[r][shape.num_layers - 1]) <= KV_ATOL_FRAC
         assert rel_err(v, ot.v_cache[r][shape.num_layers - 1]) <= KV_ATOL_FRAC
+
+
+def test_page_pool_exhaustion_is_clean():
+    """A task that needs more KV pages than are free fails with the pool untouched, and the
+    context keeps working (fp_task_create releases everything it took on any failure)."""
+    from paper_2602_16603_b200 import _lib
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    shape = F.SHAPES["tiny"]
+    w = F.make_weights(shape, 3)
+    c = PrefillContext(SHAPES["tiny"], kv_pages=8, max_pos=4096)
+    try:
+        c.load_weights(w)
+        assert c.free_pages() == 8
+        with pytest.raises(_lib.NativeError, match="exhausted"):
+            c.create_task(F.make_tokens([600, 600], shape.vocab, 1))  # 10 pages
+        assert c.free_pages() == 8
+        t = run_straight(c, F.make_tokens([900], shape.vocab, 2))
+        assert c.free_pages() == 8 - 8
+        t.destroy()
+        assert c.free_pages() == 8
+    finally:
+        c.close()
