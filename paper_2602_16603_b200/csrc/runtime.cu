@@ -940,9 +940,12 @@ extern "C" {
 const char* fp_last_error(void) { return g_err.c_str(); }
 int fp_version(void) { return 1; }
 
-int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
-                  void* nccl_comm, int64_t kv_pages, int32_t page_size, fp_ctx** out) {
-  REQ(cfg && out, "null argument");
+// Builds the context into *cp (set as soon as it exists: a failure part-way is cleaned up by
+// fp_ctx_destroy, which tolerates unset members).
+static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank,
+                           int32_t tp_size, void* nccl_comm, int64_t kv_pages, int32_t page_size,
+                           fp_ctx** cp) {
+  REQ(cfg, "null argument");
   REQ(nccl_comm == nullptr,
       "nccl_comm must be null: the tensor-parallel exchange runs over peer memory "
       "(fp_tp_connect_local / fp_tp_export + fp_tp_import)");
@@ -968,6 +971,7 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
   CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
   if (major != 10) return set_err(FP_ERR_UNSUPPORTED, "requires an sm_100 (B200) device");
   fp_ctx* c = new fp_ctx();
+  *cp = c;
   c->device = device;
   c->cfg = *cfg;
   c->tp_rank = tp_rank;
@@ -1110,6 +1114,23 @@ int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int3
     }
   }
   c->worker = std::thread(worker_main, c);
+  return FP_OK;
+}
+
+int fp_ctx_create(int32_t device, const fp_model_cfg* cfg, int32_t tp_rank, int32_t tp_size,
+                  void* nccl_comm, int64_t kv_pages, int32_t page_size, fp_ctx** out) {
+  REQ(out, "null argument");
+  fp_ctx* c = nullptr;
+  const int rc = ctx_create_impl(device, cfg, tp_rank, tp_size, nccl_comm, kv_pages, page_size, &c);
+  if (rc != FP_OK) {
+    if (c) {
+      const std::string msg = fp_last_error();  // keep the first failure's message
+      fp_ctx_destroy(c);
+      cudaGetLastError();  // a failed allocation must not surface in a later, unrelated check
+      set_err(rc, msg);
+    }
+    return rc;
+  }
   *out = c;
   return FP_OK;
 }
@@ -1146,6 +1167,7 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaFree(c->kv);
   cudaFree(c->ws);
   cudaFree(c->tickets);
+  cudaFree(c->sk_flags);
   cudaFree(c->attn_sched);
   cudaFree(c->gemm_dbg);
   cudaFreeHost((void*)c->hctl);
@@ -1155,10 +1177,8 @@ int fp_ctx_destroy(fp_ctx* c) {
   cudaFree(c->d_tp);
   if (c->stage) cudaFreeHost(c->stage);
   if (c->stage_ev) cudaEventDestroy(c->stage_ev);
-  cudaStreamDestroy(c->own_stream);
-  cudaStreamDestroy(c->upload);
-  cudaStreamDestroy(c->readback);
-  cudaStreamDestroy(c->release);
+  for (cudaStream_t st : {c->own_stream, c->upload, c->readback, c->release})
+    if (st) cudaStreamDestroy(st);
   delete c;
   return FP_OK;
 }
@@ -1671,6 +1691,7 @@ int fp_task_create(fp_ctx* c, const int32_t* ids, const int32_t* lens, int32_t n
   const int rc = task_create_impl(c, ids, lens, n_seqs, chunk_tokens, granularity, task_id, &t);
   if (rc != FP_OK) {
     if (t) task_release_partial(c, t);
+    cudaGetLastError();  // a failed allocation must not surface in a later, unrelated check
     return rc;
   }
   *out = reinterpret_cast<fp_task*>(t);

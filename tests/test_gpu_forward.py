@@ -213,3 +213,23 @@ def test_page_pool_exhaustion_is_clean():
         assert c.free_pages() == 8
     finally:
         c.close()
+
+
+def test_context_creation_failure_releases_memory():
+    """A context whose KV pool cannot be allocated fails cleanly: the weights and streams it had
+    already created are released, and the next context works."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    with pytest.raises(_lib.NativeError):
+        PrefillContext(SHAPES["llama3-8b"], kv_pages=4_000_000, max_pos=4096)  # ~2 TB of KV
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < (256 << 20), (free0, free1)  # the 16 GB of weights were freed
+    c = PrefillContext(SHAPES["tiny"], kv_pages=8, max_pos=1024)
+    c.close()
