@@ -1004,15 +1004,20 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
     CK(cudaMalloc(&ly.wqkv, (size_t)c->qkv_n * d * 2));
     CK(cudaMemset(ly.wqkv, 0, (size_t)c->qkv_n * d * 2));  // padding rows stay zero
     CK(cudaMalloc(&ly.wo, (size_t)d * c->qdim * 2));
+    CK(cudaMemset(ly.wo, 0, (size_t)d * c->qdim * 2));  // weights start zero: a partial load
     if (cfg->n_experts == 0) {
       CK(cudaMalloc(&ly.wgu, (size_t)2 * c->ffn * d * 2));
-      CK(cudaMalloc(&ly.wd, (size_t)d * c->ffn * 2));
+      CK(cudaMemset(ly.wgu, 0, (size_t)2 * c->ffn * d * 2));  // (and a norm refold of rows not
+      CK(cudaMalloc(&ly.wd, (size_t)d * c->ffn * 2));            // loaded yet) reads defined data
+      CK(cudaMemset(ly.wd, 0, (size_t)d * c->ffn * 2));
     } else {
       const size_t E = cfg->n_experts, I = cfg->moe_ffn;
       CK(cudaMalloc(&ly.wr, (size_t)256 * d * 2));
       CK(cudaMemset(ly.wr, 0, (size_t)256 * d * 2));  // padding experts: logits 0, masked
       CK(cudaMalloc(&ly.egu, E * 2 * I * d * 2));
+      CK(cudaMemset(ly.egu, 0, E * 2 * I * d * 2));
       CK(cudaMalloc(&ly.ed, E * d * I * 2));
+      CK(cudaMemset(ly.ed, 0, E * d * I * 2));
     }
     CK(cudaMalloc(&ly.attn_g, (size_t)d * 2));
     CK(cudaMalloc(&ly.ffn_g, (size_t)d * 2));
@@ -1028,6 +1033,8 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
     if (cfg->qk_norm) {
       CK(cudaMalloc(&ly.q_norm, 128 * 4));
       CK(cudaMalloc(&ly.k_norm, 128 * 4));
+      CK(cudaMemset(ly.q_norm, 0, 128 * 4));
+      CK(cudaMemset(ly.k_norm, 0, 128 * 4));
     }
     int rc;
     if ((rc = make_map(&ly.tm_qkv, ly.wqkv, c->qkv_n, d, 128))) return rc;
@@ -1043,6 +1050,7 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
     }
   }
   CK(cudaMalloc(&c->embed, (size_t)cfg->vocab * d * 2));
+  CK(cudaMemset(c->embed, 0, (size_t)cfg->vocab * d * 2));
   c->vocab_pad = (cfg->vocab + 255) / 256 * 256;  // lm_head GEMM tiles are 256 wide
   CK(cudaMalloc(&c->lm_head, (size_t)c->vocab_pad * d * 2));
   CK(cudaMemset(c->lm_head, 0, (size_t)c->vocab_pad * d * 2));
