@@ -28,7 +28,7 @@ def test_gemm(ctx, M, N, K, epi):
     B = (torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05)
     ref = A.float() @ B.float().t()
     if epi == 1:
-        out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+        out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
     else:
         out = torch.randn(M, N, device="cuda", dtype=torch.bfloat16, generator=g)
     r0 = out.float().clone()
