@@ -80,10 +80,26 @@ def config2_trace(rate: float, duration: float, seed: int = 7):
     return ps.generate_trace(classes, rate, duration, seed)
 
 
+STEP_TRACE = os.path.join(ROOT, "tests", "golden", "config2_step_trace.jsonl")
+
+
+class StepRequest:
+    __slots__ = ("id", "task", "arrival_s", "num_tokens", "ttft_slo_s")
+
+    def __init__(self, d):
+        for k in self.__slots__:
+            setattr(self, k, d[k])
+
+
 def step_requests(world: int, rank: int):
-    tr = config2_trace(8.0, 300.0)
-    reqs = [r for i, r in enumerate(tr.requests[: STEP_REQUESTS * world]) if i % world == rank]
-    return reqs
+    """The step's requests: the head of the config-2 trace (reference generate_trace, rate 8,
+    300 s, seed 7), read from the committed fixture made by tests/golden/make_golden.py so the
+    timed legs never need the reference scheduler. Request i -> rank i mod world."""
+    with open(STEP_TRACE) as fh:
+        reqs = [StepRequest(json.loads(ln)) for ln in fh if ln.strip()]
+    if len(reqs) < STEP_REQUESTS * world:
+        raise ValueError(f"{STEP_TRACE} holds {len(reqs)} requests, need {STEP_REQUESTS * world}")
+    return [r for i, r in enumerate(reqs[: STEP_REQUESTS * world]) if i % world == rank]
 
 
 class ClockSampler:
@@ -264,6 +280,13 @@ def run_ours(args):
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         return float(v.item())
 
+    def sum_over_ranks(x: int) -> int:
+        if dist is None:
+            return x
+        v = torch.tensor([x], dtype=torch.int64, device=f"cuda:{device}")
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        return int(v.item())
+
     for _ in range(max(args.warmup, 1)):
         run_step()
     ctx.sync()
@@ -289,7 +312,8 @@ def run_ours(args):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     ms_max = max_over_ranks(ms)
-    total_tokens = step_tokens * args.steps * ws  # weak scaling: every rank did its share
+    job_step_tokens = sum_over_ranks(step_tokens)  # ranks hold different requests
+    total_tokens = job_step_tokens * args.steps
     value = total_tokens / (ms_max / 1e3)
 
     # -------- per-kernel CUDA events (same steps again, events around every kernel; the
@@ -380,10 +404,13 @@ def run_ours(args):
     d2h //= e2e_steps
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     barrier()
-    e2e_value = step_tokens * e2e_steps * ws / e2e_s
+    e2e_value = job_step_tokens * e2e_steps / e2e_s
 
     # -------- p99 preemption latency on a long request (async launch worker)
-    pre = preemption_latency(ctx, shape, rank)
+    try:
+        pre = preemption_latency(ctx, shape, rank)
+    except Exception as e:  # keep the bench line; record why the leg failed
+        pre = {"error": repr(e)[:300]}
 
     # -------- goodput: reference goodput_search on the B200-calibrated cost model
     good = None
@@ -406,8 +433,11 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:
         v, cores, sample = cpu_sample()
-        cpu = {"value": v, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample,
-               "control_plane": control_plane_time()}
+        cpu = {"value": v, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample}
+        try:
+            cpu["control_plane"] = control_plane_time()
+        except Exception as e:  # the reference scheduler is absent on this host
+            cpu["control_plane"] = {"error": repr(e)[:200]}
 
     for t in tasks:
         t.destroy()
@@ -674,8 +704,24 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     else:
         run_ours(args)
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch as N ranks (one per GPU) the way the
+    driver does, so the line always measures N GPUs and reports n_gpus = N."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 if __name__ == "__main__":

@@ -165,6 +165,9 @@ struct Task {
   // host execution state
   int gen = 0, seg_first = 0, enq = 0, seg_ack0 = 0, done_recorded = 0;
   std::atomic<int> worker_active{0};
+  // sticky launch failure of the async worker (fp_task_poll reports it; the task is dead)
+  std::atomic<int> err{0};
+  std::string err_msg;
 };
 
 struct fp_ctx {
@@ -276,6 +279,16 @@ struct ProfScope {
 };
 
 // --------------------------------------------------------------------------- launches
+// Kernel attributes (max dynamic shared memory) are per device: a process with contexts on
+// several GPUs sets them per (kernel, device). The bit is published only after the attribute
+// is set (concurrent first launches both set it, which is harmless).
+template <typename F>
+static void once_per_device(std::atomic<unsigned long long>& mask, int dev, F&& set) {
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return;
+  set();
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+}
 // Every kernel is launched with programmatic stream serialisation: its prologue (barrier init,
 // TMEM alloc, descriptor prefetch) may start while the previous kernel drains; the kernel
 // itself waits (griddepcontrol.wait) before its boundary check and any data access.
@@ -351,15 +364,14 @@ template <int EPI, int CG, int BN = 256>
 static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b, GemmParams p,
                            cudaStream_t st) {
   using Cfg = GemmCfg<BN, CG>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};  // per device (the attribute is per device)
+  once_per_device(attr, c->device, [] {
     cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI, CG, 0>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if constexpr (BN == 256)
       cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI, CG, 1>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    attr = true;
-  }
+  });
   const int tiles = ((p.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * (p.N / BN);
   const int slots = c->num_sms / CG;  // concurrent tiles (CTA pairs)
   p.group_m = raster_group(c, p);
@@ -419,11 +431,10 @@ static void launch_gemm_grouped(fp_ctx* c, const CUtensorMap& a, const CUtensorM
                                 GemmParams p, cudaStream_t st) {
   using Cfg = GemmCfg<256, 1>;
   auto kern = gemm_bf16_tn_kernel<256, EPI, 1, 2>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, c->device, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    attr = true;
-  }
+  });
   p.splits = 1;
   p.full_tiles = 0;
   launch_pdl(kern, dim3(c->num_sms), dim3(kGemmThreads), Cfg::SMEM_BYTES, st, a, b, p);
@@ -512,11 +523,10 @@ static void launch_gemm_sk(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
                            cudaStream_t st, const SkPlan& pl) {
   using Cfg = GemmCfg<256, 1>;
   auto kern = gemm_bf16_tn_kernel<256, EPI, 1, 3>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, c->device, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SK_SMEM_BYTES);
-    attr = true;
-  }
+  });
   p.splits = 1;
   p.full_tiles = pl.dp_tiles;
   p.group_m = raster_group(c, p);
@@ -576,12 +586,11 @@ static int launch_rms(const RmsParams& p, cudaStream_t st) {
 
 static void launch_attn(const fp_ctx* c, const CUtensorMap& tq, const CUtensorMap& tkv,
                         const AttnTcParams& p, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, c->device, [] {
     cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          tcattn::SMEM_BYTES);
-    attr = true;
-  }
+  });
   // persistent: one CTA per SM (at most one per work item), work taken longest-first
   const int n_work = p.n_items * p.n_kv_heads * p.pairs_per_kv;
   launch_pdl(attn_prefill_tc_kernel, dim3(std::min(n_work, c->num_sms)), dim3(tcattn::THREADS),
@@ -897,6 +906,17 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
   return FP_OK;
 }
 
+// launch_entry plus the launch status: cudaLaunchKernelEx failures (bad config, missing
+// attribute, sticky device error) surface here instead of a silently skipped kernel.
+static int launch_entry_checked(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
+  int rc = launch_entry(c, t, e, phase);
+  const cudaError_t le = cudaGetLastError();
+  if (rc == FP_OK && le != cudaSuccess)
+    rc = set_err(FP_ERR_CUDA, std::string("kernel launch of entry ") + std::to_string(e) + ": " +
+                                  cudaGetErrorString(le));
+  return rc;
+}
+
 // --------------------------------------------------------------------------- worker
 static void worker_main(fp_ctx* c) {
   cudaSetDevice(c->device);
@@ -914,7 +934,12 @@ static void worker_main(fp_ctx* c) {
       if (c->hctl->progress_task == t->id) prog = std::max(prog, (int)c->hctl->progress_entry);
       if (t->enq - prog <= c->window) {
         std::lock_guard<std::mutex> lk(c->launch_mu);
-        launch_entry(c, t, t->enq);
+        const int rc = launch_entry_checked(c, t, t->enq);
+        if (rc) {  // stop launching; never report this segment done
+          t->err_msg = g_err;
+          t->err.store(rc);
+          break;
+        }
         t->enq++;
       } else {
         std::this_thread::yield();
@@ -922,9 +947,11 @@ static void worker_main(fp_ctx* c) {
     }
     {
       std::lock_guard<std::mutex> lk(c->launch_mu);
-      cudaEventRecord(t->done, c->stream);
+      if (!t->err.load() && t->enq == t->n_entries) {
+        cudaEventRecord(t->done, c->stream);
+        t->done_recorded = 1;
+      }
       cudaEventRecord(t->fence, c->stream);
-      t->done_recorded = 1;
     }
     {
       std::lock_guard<std::mutex> lk(c->wmu);
@@ -1804,7 +1831,7 @@ int fp_task_enqueue(fp_ctx* c, fp_task* task, int32_t first, int32_t last) {
   CK(cudaSetDevice(c->device));
   std::lock_guard<std::mutex> lk(c->launch_mu);
   for (int e = first; e < last; ++e) {
-    int rc = launch_entry(c, t, e);
+    int rc = launch_entry_checked(c, t, e);
     if (rc) return rc;
   }
   t->enq = std::max(t->enq, (int)last);
@@ -1838,6 +1865,7 @@ int fp_task_start(fp_ctx* c, fp_task* task, int32_t first) {
 int fp_task_poll(fp_ctx* c, fp_task* task, fp_task_status* st) {
   Task* t = reinterpret_cast<Task*>(task);
   REQ(c && t && st, "null argument");
+  if (int e = t->err.load()) return set_err(e, "async launch failed: " + t->err_msg);
   st->generation = t->gen;
   st->enqueued = t->enq;
   const int ack_seq = c->hctl->ack_seq;
@@ -2348,7 +2376,7 @@ int fp_tp_enqueue_lockstep(fp_ctx** ctxs, fp_task** tasks, int32_t n, int32_t fi
   for (int e = first; e < last; ++e)
     for (int phase : {kPhasePre, kPhasePost})
       for (int r = 0; r < n; ++r) {  // rank 0 first: its boundary decision precedes the others'
-        int rc = launch_entry(ctxs[r], ts[r], e, phase);
+        int rc = launch_entry_checked(ctxs[r], ts[r], e, phase);
         if (rc) return rc;
       }
   for (int r = 0; r < n; ++r) {

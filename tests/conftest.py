@@ -31,3 +31,14 @@ def pytest_collection_modifyitems(config, items):
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
+
+
+def refsim_or_skip():
+    """The reference prefillsim package (baseline/_ref on the GPU box, installed by
+    __graft_entry__.build()); skip, with the reason, when this host has no copy."""
+    from paper_2602_16603_b200 import refsim
+
+    try:
+        return refsim.load()
+    except ImportError as e:
+        pytest.skip(str(e))

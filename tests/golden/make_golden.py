@@ -192,6 +192,23 @@ def reference_events() -> None:
     res.write_event_log(os.path.join(HERE, "config1_events.jsonl"))
     workload.save_trace(tr, os.path.join(HERE, "config1_trace.jsonl"))
     print("config1:", len(tr), "requests", res.commands)
+    config2_step_trace()
+
+
+def config2_step_trace() -> None:
+    """bench.py's step workload: the first 128 requests (16 per GPU x 8 GPUs) of the config-2
+    3-class trace (text 0.76 @0.25 s, search 0.20 @4.0 s, file 0.04 @6.0 s), made by
+    the reference generate_trace (workload.py:162-198, rate 8, 300 s, seed 7). Committed so the
+    bench's timed legs never import the reference."""
+    from prefillsim import workload
+
+    classes = [workload.TaskClass("text", 590.0, 652.0, 3040.0, 0.76, 0.25),
+               workload.TaskClass("search", 5976.0, 3456.0, 16635.0, 0.20, 4.0),
+               workload.TaskClass("file", 6833.0, 5186.0, 22390.0, 0.04, 6.0)]
+    tr = workload.generate_trace(classes, 8.0, 300.0, seed=7)
+    head = workload.Trace(tuple(tr.requests[:128]))
+    workload.save_trace(head, os.path.join(HERE, "config2_step_trace.jsonl"))
+    print("config2 step trace:", [r.num_tokens for r in head.requests[:16]])
 
 
 def main() -> None:
@@ -222,6 +239,12 @@ def main() -> None:
 if __name__ == "__main__":
     if "--moe" in sys.argv:
         moe_golden()
+    elif "--config2" in sys.argv:
+        for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+            if os.path.isdir(os.path.join(p, "prefillsim")):
+                sys.path.insert(0, p)
+                break
+        config2_step_trace()
     else:
         main()
         moe_golden()

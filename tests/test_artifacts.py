@@ -2,6 +2,7 @@
 run.csv / summary.json / sweep.csv and the reference goodput bisection over a round-robin
 deployment. At one instance every artifact must be byte-identical to the reference CLI's."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import filecmp
 import json
 import os
@@ -15,7 +16,7 @@ TRACE = os.path.join(GOLDEN, "config1_trace.jsonl")
 def _ps():
     from paper_2602_16603_b200 import refsim
 
-    return refsim.load()
+    return refsim_or_skip()
 
 
 def test_single_instance_artifacts_match_reference_cli(tmp_path):
@@ -104,7 +105,7 @@ def _worker(rank, world, port, out_dir):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ps = refsim.load()
+    ps = refsim_or_skip()
     tr = ps.load_trace(TRACE)
     mine = dispatch.round_robin(tr, world)[rank]
     local = ps.run(mine, ps.PolicyConfig(), ps.CostParams(num_layers=4), 0)

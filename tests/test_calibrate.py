@@ -3,6 +3,7 @@ CostParams from profile records in the live-profile format, charges pre-GEMM nor
 following entry and the final norm + lm_head to the chunk, and its predictions go through the
 reference's own operator_duration (cost_model.py:151-166)."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import numpy as np
 
 from paper_2602_16603_b200 import refsim
@@ -31,7 +32,7 @@ def records(lens, norm_ms=0.004, extra_ms=0.25, noise=0.0, seed=0):
 
 
 def test_fit_recovers_known_cost_params():
-    ps = refsim.load()
+    ps = refsim_or_skip()
     lens = [1, 42, 163, 545, 1572, 4465]
     recs = records(lens)
     samples = entry_samples(recs)
@@ -48,7 +49,7 @@ def test_fit_recovers_known_cost_params():
 def test_fit_is_relative_error_weighted():
     """With noisy long entries, the short entries are still predicted within a few percent
     (an absolute least-squares fit would trade them for the long ones)."""
-    ps = refsim.load()
+    ps = refsim_or_skip()
     lens = [40, 80, 160, 320, 640, 1280, 2560, 5120]
     recs = records(lens, noise=0.02, seed=3)
     p = fit_cost_params(recs, num_layers=32)

@@ -2,6 +2,7 @@
 world_size 2 gloo ranks, each running its own scheduler + execution pool with no data-path
 collective, outcomes gathered for the metrics."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import os
 
 import pytest
@@ -10,7 +11,7 @@ import pytest
 def test_round_robin_partition():
     from paper_2602_16603_b200 import dispatch, refsim
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     tr = ps.load_trace(os.path.join(os.path.dirname(__file__), "golden", "config1_trace.jsonl"))
     parts = dispatch.round_robin(tr, 3)
     assert sum(len(p) for p in parts) == len(tr)
@@ -29,7 +30,7 @@ def _worker(rank, world, port, q):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ps = refsim.load()
+    ps = refsim_or_skip()
     tr = ps.load_trace(os.path.join(os.path.dirname(__file__), "golden", "config1_trace.jsonl"))
     mine = dispatch.round_robin(tr, world)[rank]
     local = ps.run(mine, ps.PolicyConfig(), ps.CostParams(num_layers=4), 0).outcomes
@@ -57,7 +58,7 @@ def test_gloo_two_instances():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ps = refsim.load()
+    ps = refsim_or_skip()
     tr = ps.load_trace(os.path.join(os.path.dirname(__file__), "golden", "config1_trace.jsonl"))
     expect = dispatch.merge_outcomes(
         [ps.run(p, ps.PolicyConfig(), ps.CostParams(num_layers=4), 0).outcomes

@@ -3,6 +3,7 @@ the reference run() with GpuEngine injected reproduces the reference goldens byt
 every timeline entry executes exactly once across preemptions, stops land on the reference
 cursor, and preempted+resumed logits equal uninterrupted ones."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import json
 import os
 
@@ -21,7 +22,7 @@ def _events(res):
 def ps():
     from paper_2602_16603_b200 import refsim
 
-    return refsim.load()
+    return refsim_or_skip()
 
 
 def test_config1_golden_through_gpu_engine(ps, golden_dir):

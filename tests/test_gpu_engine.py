@@ -2,6 +2,7 @@
 byte-identical to the reference goldens, every device-side stop must land on the reference
 cursor, and the logits of every request must match the fp32 oracle (bf16 tolerance)."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import json
 import os
 
@@ -23,7 +24,7 @@ def test_config1_trace_parity(golden_dir):
     from paper_2602_16603_b200.engine import GpuBinding, run_on_gpu, synthetic_tokens
     from paper_2602_16603_b200.native import PrefillContext
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     trace = ps.load_trace(os.path.join(golden_dir, "config1_trace.jsonl"))
     shape = F.SHAPES["tiny"]
     w = F.make_weights(shape, 1234)
@@ -58,7 +59,7 @@ def test_two_request_golden_llama3_8b(golden_dir):
     from paper_2602_16603_b200.engine import GpuBinding, run_on_gpu, synthetic_tokens
     from paper_2602_16603_b200.native import PrefillContext
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     shape = SHAPES["llama3-8b"]
     ctx = PrefillContext(shape, kv_pages=96, page_size=128, max_pos=16384)
     ctx.init_random(seed=0)

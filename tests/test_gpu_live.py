@@ -1,5 +1,6 @@
 """Wall-clock driver on the B200: reference scheduler + real asynchronous preemption."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import os
 
 import numpy as np
@@ -16,7 +17,7 @@ def test_live_config1_trace(golden_dir):
     from paper_2602_16603_b200.live import run_live
     from paper_2602_16603_b200.native import PrefillContext
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     trace = ps.load_trace(os.path.join(golden_dir, "config1_trace.jsonl"))
     trace = ps.scale_rate(trace, 10.0)  # 45 requests in ~2 s of wall time
     shape = F.SHAPES["tiny"]
@@ -48,7 +49,7 @@ def test_live_preemption_llama_shape():
     from paper_2602_16603_b200.live import run_live
     from paper_2602_16603_b200.native import PrefillContext
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     shape = replace(SHAPES["llama3-8b"], num_layers=4)
     ctx = PrefillContext(shape, kv_pages=256, max_pos=40000)
     ctx.init_random(0)

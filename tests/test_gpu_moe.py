@@ -16,6 +16,7 @@ weights of agreeing tokens must be within 0.05; GPU-vs-GPU comparisons (preempte
 repeated runs) are bit-exact.
 """
 
+from conftest import refsim_or_skip  # noqa: E402
 import numpy as np
 import pytest
 
@@ -174,7 +175,7 @@ def test_moe_reference_event_log(moe):
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.engine import GpuBinding, run_on_gpu, synthetic_tokens
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     shape, w, ctx = moe
     params = ps.CostParams(num_layers=shape.num_layers, arch="moe")
     trace = ps.Trace((ps.Request(0, "file", 0.0, 900, 6.0), ps.Request(1, "text", 0.0004, 64, 0.25),

@@ -11,6 +11,7 @@ bf16 before the exchange). Replicated state (logits, residual) is bit-identical 
 preempted vs straight runs are bit-identical.
 """
 
+from conftest import refsim_or_skip  # noqa: E402
 import json
 
 import numpy as np
@@ -183,7 +184,7 @@ def test_tp_reference_run_config1(golden_dir):
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.engine import GpuBinding, run_on_gpu, synthetic_tokens
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     trace = ps.load_trace(os.path.join(golden_dir, "config1_trace.jsonl"))
     shape = F.SHAPES[NAME]
     w = F.make_weights(shape, 4321)
@@ -213,7 +214,7 @@ def test_qwen25_32b_shape_tp_reference_parity(tp):
     from paper_2602_16603_b200.engine import GpuBinding, run_on_gpu, synthetic_tokens
     from paper_2602_16603_b200.native import TPGroup
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     shape = SHAPES["qwen2.5-32b"]
     trace = ps.Trace((ps.Request(0, "file", 0.0, 6000, 6.0), ps.Request(1, "text", 0.05, 300, 0.25)))
     params = ps.CostParams(num_layers=64, tp_degree=tp)

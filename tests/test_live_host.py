@@ -2,6 +2,7 @@
 arrival plus one per task completion (test_properties.py:80-84), every preemption is ACKed and
 resumed from the device cursor, blocking is bounded by one entry + polling slack."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import os
 
 import numpy as np
@@ -15,7 +16,7 @@ def test_live_driver_invariants(gran):
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.live import run_live
 
-    ps = refsim.load()
+    ps = refsim_or_skip()
     # a long request followed by urgent short ones, replayed in ~0.1 s of wall time
     reqs = [ps.Request(0, "file", 0.0, 4000, 10.0)]
     for i in range(1, 9):

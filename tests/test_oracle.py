@@ -2,6 +2,7 @@
 HF transformers Llama logits (golden), the reference's own build_timeline / known answers,
 and the reference's own run() goldens."""
 
+from conftest import refsim_or_skip  # noqa: E402
 import json
 import os
 
@@ -15,7 +16,7 @@ from oracle import forward as F
 def ps():
     from paper_2602_16603_b200 import refsim
 
-    return refsim.load()
+    return refsim_or_skip()
 
 
 def test_oracle_matches_hf_golden(golden_dir):
