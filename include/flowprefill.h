@@ -151,6 +151,11 @@ typedef struct fp_task_info {
 int fp_task_info(const fp_task* task, fp_task_info_t* info);
 int fp_task_entry_info(const fp_task* task, int32_t entry, int32_t* chunk, int32_t* layer,
                        int32_t* op, int32_t* new_tokens);
+/* %globaltimer (ns) at each entry's boundary decision: host_out[e] = GO (0: not executed yet),
+ * host_out[n_entries + e] = STOP (0: never stopped there). Entry e-1 ends at entry e's STOP if
+ * there was one, else at its GO: the wall-clock form of OperatorTimeline.max_entry_duration
+ * (cost_model.py:185-188), the bound on signal -> ACK blocking (test_properties.py:90-94). */
+int fp_task_entry_stamps(fp_ctx* ctx, fp_task* task, uint64_t* host_out); /* [2, n_entries] */
 int fp_task_destroy(fp_ctx* ctx, fp_task* task);
 
 /* Start a new execution segment from `first` (Engine.submit / Engine.resume,

@@ -145,6 +145,7 @@ _SIGS = {
     "fp_clear": (C.c_int, [_P]),
     "fp_poll": (C.c_int, [_P, C.POINTER(Status)]),
     "fp_task_logits": (C.c_int, [_P, _P, _P]),
+    "fp_task_entry_stamps": (C.c_int, [_P, _P, _P]),
     "fp_task_read_kv": (C.c_int, [_P, _P, _I, _I, _P, _P]),
     "fp_prof_enable": (C.c_int, [_P, _I]),
     "fp_prof_collect": (C.c_int, [_P, C.POINTER(ProfRec), _I, C.POINTER(_I)]),

@@ -26,7 +26,9 @@ struct HostCtl {
 // Device memory: one per task. dec[] holds one decision per timeline entry.
 struct TaskCtl {
   int stopped_gen;  // generation that has been stopped (-1: none)
-  int pad[31];
+  int pad0;
+  unsigned long long* stamps;  // [2][n_entries] %globaltimer at each entry's GO / STOP decision
+  int pad[28];
   int dec[1];       // [n_entries]: 0 undecided, 1 go, 2 stop
 };
 
@@ -77,7 +79,7 @@ struct Guard {
   int task_id;
   int first;     // 1 for the first kernel of the entry: evaluates the check
   int eligible;  // the boundary in front of this entry is preemption-eligible
-  int pad;
+  int n_entries;
   const TpDev* tp;  // null unless tensor parallel
 };
 
@@ -141,10 +143,12 @@ DEVI bool guard_pass(const Guard& g) {
       g.host->ack_task = g.task_id;
       g.host->ack_entry = g.entry;
       g.host->ack_ns = globaltimer();
+      if (g.task->stamps) g.task->stamps[g.n_entries + g.entry] = g.host->ack_ns;
       __threadfence_system();
       g.host->ack_seq = g.host->ack_seq + 1;
       __threadfence_system();
     } else {
+      if (g.task->stamps) g.task->stamps[g.entry] = globaltimer();
       g.host->progress_task = g.task_id;
       g.host->progress_entry = g.entry;
       __threadfence_system();

@@ -151,6 +151,7 @@ struct Task {
   float* ssq;  // [max_m, hidden/128] segment sums of squares of h (fused RMSNorm input)
   float* logits;
   TaskCtl* ctl;
+  unsigned long long* stamps = nullptr;  // inside the ctl allocation
   CUtensorMap tm_h, tm_ao, tm_act, tm_xf, tm_q;
   // MoE routing state of the current chunk (gate -> experts) and expert-ordered buffers
   float* rlog = nullptr;                       // [max_m, 256] router logits
@@ -767,6 +768,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
   g.task_id = t->id;
   g.first = 1;
   g.eligible = (e != t->seg_first) && boundary_eligible(c, t->granularity, e - 1, t->n_entries);
+  g.n_entries = t->n_entries;
   g.tp = c->d_tp;
   Guard g2 = g;
   g2.first = 0;
@@ -1648,10 +1650,14 @@ static int task_create_impl(fp_ctx* c, const int32_t* ids, const int32_t* lens, 
   CK(cudaMallocAsync((void**)&t->xf, (long long)n_seqs * d * 2, up));
   CK(cudaMallocAsync((void**)&t->logits, (long long)n_seqs * c->vocab_pad * 4, up));
   CK(cudaMemsetAsync(t->logits, 0, (long long)n_seqs * c->vocab_pad * 4, up));
-  const size_t ctl_bytes = sizeof(TaskCtl) + (size_t)t->n_entries * 4;
+  // decision slots, then the per-entry GO timestamps (entry durations for the blocking bound)
+  const size_t stamp_off = (sizeof(TaskCtl) + (size_t)t->n_entries * 4 + 15) & ~(size_t)15;
+  const size_t ctl_bytes = stamp_off + (size_t)t->n_entries * 16;
   CK(cudaMallocAsync((void**)&t->ctl, ctl_bytes, up));
   CK(cudaMemsetAsync(t->ctl, 0, ctl_bytes, up));
   CK(cudaMemsetAsync(&t->ctl->stopped_gen, 0xFF, 4, up));  // -1
+  t->stamps = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(t->ctl) + stamp_off);
+  CK(cudaMemcpyAsync(&t->ctl->stamps, &t->stamps, sizeof(t->stamps), cudaMemcpyHostToDevice, up));
   int rc;
   if ((rc = make_map(&t->tm_h, t->h, M, d, 128))) return rc;
   if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
@@ -1759,6 +1765,17 @@ int fp_task_entry_info(const fp_task* task, int32_t e, int32_t* chunk, int32_t* 
   if (layer) *layer = (e / 5) % t->L;
   if (op) *op = e % 5;
   if (new_tokens) *new_tokens = t->chunks[ci].M;
+  return FP_OK;
+}
+
+int fp_task_entry_stamps(fp_ctx* c, fp_task* task, uint64_t* host_out) {
+  Task* t = reinterpret_cast<Task*>(task);
+  REQ(c && t && host_out, "null argument");
+  CK(cudaSetDevice(c->device));
+  // a snapshot: entries still running publish their stamps later
+  CK(cudaMemcpyAsync(host_out, t->stamps, (size_t)t->n_entries * 16, cudaMemcpyDeviceToHost,
+                     c->readback));
+  CK(cudaStreamSynchronize(c->readback));
   return FP_OK;
 }
 

@@ -52,10 +52,15 @@ def run_live(
     record_events: bool = False,
     time_scale: float = 1.0,
     max_wall_s: Optional[float] = None,
+    round_log: Optional[list] = None,
 ) -> RunResult:
     """Replay ``trace`` in real time on ``ctx``. ``cost_params`` only shapes the timeline
     bookkeeping (progress weights) and, when ``predictor`` is None, the reference's
-    self-calibrated TTFT predictor; pass B200-calibrated params (calibrate.py)."""
+    self-calibrated TTFT predictor; pass B200-calibrated params (calibrate.py).
+
+    ``round_log`` (a list) receives one record per scheduling round -- its wall time, the
+    arrivals and completions it consumes, the cursor of every live task as the scheduler saw
+    it, and the commands it returned -- for ``replay_rounds`` (SURVEY.md §7 hard part 5)."""
     if predictor is None:
         predictor = ps.self_calibrated_poly(
             cost_params, degree=policy_config.predictor_degree,
@@ -82,12 +87,30 @@ def run_live(
         if events is not None:
             events.append({"t": t, "kind": kind, "task": task, "detail": detail})
 
-    def do_round(t, arrivals):
-        nonlocal rounds
+    noted: list = []  # completions noted since the last round (note_completion order)
+
+    def note(task_id):
+        state.note_completion(task_id)
+        noted.append(task_id)
+
+    def do_round(t, arrivals, trigger):
+        nonlocal rounds, noted
         rounds += 1
         if running is not None:
             running.refresh()
-        execute(schedule_round(state, t, arrivals), t)
+        if round_log is not None:
+            live = [running] if running is not None else []
+            live += [x for x in state.q_preempted.values()]
+            rec = {"round": rounds, "t": t, "trigger": trigger,
+                   "arrivals": [r.id for r in arrivals], "completions": noted,
+                   "cursors": {x.task_id: x.cursor for x in live},
+                   "running": running.task_id if running is not None else None}
+        noted = []
+        cmds = schedule_round(state, t, arrivals)
+        if round_log is not None:
+            rec["commands"] = [command_key(c) for c in cmds]
+            round_log.append(rec)
+        execute(cmds, t)
 
     def execute(cmds, t):
         nonlocal followup, pending_signal, signal_t
@@ -141,7 +164,7 @@ def run_live(
         if pending_signal:
             buffered.append(("arrival", req))
         else:
-            do_round(t, [req])
+            do_round(t, [req], "arrival")
 
     def finish(task, t):
         for r in task.member_requests:
@@ -151,6 +174,10 @@ def run_live(
         task.cursor = len(task)
         task.state = ps.TaskState.DONE
         log("completion", task.task_id, t, requests=[r.id for r in task.member_requests])
+        if round_log is not None:
+            # measured longest entry (device stamps): the task's wall-clock blocking bound
+            round_log.append({"done": task.task_id, "t": t,
+                              "max_entry_s": task.native.max_entry_s()})
         task.native.destroy()
 
     def on_completion(task, t):
@@ -160,8 +187,8 @@ def run_live(
         if pending_signal:
             buffered.append(("completion", task.task_id))
         else:
-            state.note_completion(task.task_id)
-            do_round(t, [])
+            note(task.task_id)
+            do_round(t, [], "completion")
 
     def on_ack(task, cursor, t):
         nonlocal running, pending_signal, followup
@@ -172,6 +199,8 @@ def run_live(
         task.generation += 1
         blocking.append((signal_t, t, task.task_id))
         log("preempt_ack", task.task_id, t, blocking_s=t - signal_t, cursor=cursor)
+        if round_log is not None:
+            round_log.append({"ack": task.task_id, "t": t, "cursor": cursor})
         pending, followup = followup, []
         run_now(pending, t)
         drain_buffer(t)
@@ -180,10 +209,10 @@ def run_live(
         while buffered and not pending_signal:
             kind, payload = buffered.popleft()
             if kind == "arrival":
-                do_round(t, [payload])
+                do_round(t, [payload], "deferred_arrival")
             else:
-                state.note_completion(payload)
-                do_round(t, [])
+                note(payload)
+                do_round(t, [], "deferred_completion")
 
     reqs = list(trace.requests)
     i = 0
@@ -204,6 +233,9 @@ def run_live(
                     blocking.append((signal_t, t, task.task_id))
                     log("preempt_ack", task.task_id, t, blocking_s=t - signal_t,
                         cursor=len(task))
+                    if round_log is not None:
+                        round_log.append({"ack": task.task_id, "t": t, "cursor": len(task),
+                                          "completed": True})
                     buffered.append(("completion", task.task_id))
                     pending, followup = followup, []
                     run_now(pending, t)
@@ -243,3 +275,87 @@ def run_live(
         granularity=policy_config.granularity.value,
         events=events,
     )
+
+
+def command_key(c) -> list:
+    """A scheduler ``Command`` (scheduler.py:118-125) as plain data: kind, task, member ids,
+    aggregate tokens."""
+    return [c.kind, c.task_id, [r.id for r in c.members], c.agg_tokens]
+
+
+def replay_rounds(trace, policy_config, cost_params, round_log: list, predictor=None) -> dict:
+    """Replay a live run's scheduling rounds through a FRESH reference ``SchedulerState`` and
+    ``schedule_round`` (scheduler.py:175-245) and check the live driver's protocol against the
+    reference ``run()`` semantics (engine.py:419-502). SURVEY.md §7 hard part 5.
+
+    Every round is re-evaluated at its logged wall time with the logged arrivals, the
+    completions noted before it, and each live task's cursor as the scheduler saw it (tasks
+    are fresh reference ``ExecutionTask`` objects over ``build_timeline``); the commands must
+    be identical. The log must also show: every request arriving exactly once; no round and
+    no submit/resume between a preempt signal and its ACK; rounds deferred by an outstanding
+    signal running at the ACK instant; every ACK cursor an eligible boundary of the task's
+    granularity (engine.py:127-134) at or after the cursor the preempting round saw.
+    Returns counts; raises ``AssertionError`` on the first mismatch."""
+    if predictor is None:
+        predictor = ps.self_calibrated_poly(
+            cost_params, degree=policy_config.predictor_degree,
+            chunk_size=policy_config.chunk_tokens)
+    state = SchedulerState.create(policy_config, predictor)
+    by_id = {r.id: r for r in trace.requests}
+    tasks: dict = {}
+    seen: set = set()
+    gran = policy_config.granularity
+    outstanding = None  # (victim task id, cursor seen by the preempting round)
+    last_ack_t = None
+    last_t = -1.0
+    n_rounds = n_cmds = n_acks = 0
+    for rec in round_log:
+        assert rec["t"] >= last_t, f"time went backwards at {rec}"
+        last_t = rec["t"]
+        if "done" in rec:
+            continue
+        if "ack" in rec:
+            assert outstanding is not None and outstanding[0] == rec["ack"], \
+                f"ACK without an outstanding signal: {rec}"
+            task = tasks[rec["ack"]]
+            cur = rec["cursor"]
+            if not rec.get("completed"):
+                assert 0 < cur < len(task), f"ACK cursor out of range: {rec}"
+                assert task.boundary_eligible(cur - 1, gran), \
+                    f"ACK at a boundary {gran.value} granularity does not allow: {rec}"
+            assert cur >= outstanding[1], f"ACK cursor before the signalled cursor: {rec}"
+            task.cursor = cur
+            outstanding = None
+            last_ack_t = rec["t"]
+            n_acks += 1
+            continue
+        assert outstanding is None, f"round {rec['round']} ran while an ACK was outstanding"
+        n_rounds += 1
+        assert rec["round"] == n_rounds, f"round numbering gap at {rec['round']}"
+        if rec["trigger"].startswith("deferred"):
+            assert rec["t"] == last_ack_t, f"deferred round not at the ACK instant: {rec}"
+        for tid in rec["completions"]:
+            state.note_completion(tid)
+        for tid, cur in rec["cursors"].items():
+            tasks[int(tid)].cursor = cur
+        arrivals = [by_id[i] for i in rec["arrivals"]]
+        for i in rec["arrivals"]:
+            assert i not in seen, f"request {i} arrived twice"
+            seen.add(i)
+        cmds = schedule_round(state, rec["t"], arrivals)
+        got = [command_key(c) for c in cmds]
+        assert got == rec["commands"], \
+            f"round {rec['round']} at t={rec['t']}: replay {got} != live {rec['commands']}"
+        n_cmds += len(cmds)
+        for c in cmds:
+            if c.kind == "preempt":
+                outstanding = (c.task_id, tasks[c.task_id].cursor)
+            elif c.kind == "submit":
+                tl = ps.build_timeline([r.num_tokens for r in c.members],
+                                       policy_config.chunk_tokens, cost_params)
+                task = ExecutionTask(c.task_id, c.members, tl)
+                tasks[c.task_id] = task
+                state.attach_task(task)
+    assert outstanding is None, "run ended with an outstanding preempt signal"
+    assert seen == set(by_id), f"requests never arrived: {sorted(set(by_id) - seen)[:10]}"
+    return {"rounds": n_rounds, "commands": n_cmds, "acks": n_acks, "tasks": len(tasks)}

@@ -271,6 +271,30 @@ class PrefillTask:
         _lib.check(self.lib.fp_task_logits(self.ctx.h, self.h, out.ctypes.data), "fp_task_logits")
         return out
 
+    def entry_stamps(self) -> np.ndarray:
+        """Device %globaltimer (ns) per entry: row 0 = GO decision (0: not executed), row 1 =
+        STOP decision at that boundary (0: never stopped there)."""
+        out = np.zeros((2, self.n_entries), np.uint64)
+        _lib.check(self.lib.fp_task_entry_stamps(self.ctx.h, self.h, out.ctypes.data),
+                   "fp_task_entry_stamps")
+        return out
+
+    def entry_durations_s(self) -> np.ndarray:
+        """Executed duration of entries 0 .. n-2 in seconds (NaN where unknown): entry e-1
+        ends at the STOP decision of boundary e if the task was stopped there, else at entry
+        e's GO decision. The last entry has no successor boundary and is not covered."""
+        go, stop = self.entry_stamps().astype(np.int64)
+        end = np.where(stop[1:] > 0, stop[1:], go[1:])
+        d = (end - go[:-1]).astype(np.float64) * 1e-9
+        d[(go[:-1] == 0) | (end == 0)] = np.nan
+        return d
+
+    def max_entry_s(self) -> float:
+        """Longest executed entry of this task (the wall-clock max_entry_duration,
+        cost_model.py:185-188)."""
+        d = self.entry_durations_s()
+        return float(np.nanmax(d)) if np.isfinite(d).any() else 0.0
+
     def routing(self) -> tuple[np.ndarray, np.ndarray]:
         """MoE tap: (expert ids, weights) [rows, top_k] of the most recent gate entry."""
         sh = self.ctx.shape

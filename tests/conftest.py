@@ -42,3 +42,24 @@ def refsim_or_skip():
         return refsim.load()
     except ImportError as e:
         pytest.skip(str(e))
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """PARITY_REPORT=<path>: write every bf16-vs-fp32 parity check of the session (max-abs and
+    relative error per config, tests/parity.py) as JSON."""
+    path = os.environ.get("PARITY_REPORT")
+    if not path:
+        return
+    try:
+        import parity
+    except ImportError:
+        return
+    import json
+
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with open(path, "w") as fh:
+        json.dump({"tolerances": {"logits": {"max_abs_frac": parity.LOGIT_ATOL_FRAC,
+                                             "rel_l2": parity.LOGIT_REL_TOL},
+                                  "kv": {"max_abs_frac": parity.KV_ATOL_FRAC,
+                                         "rel_l2": parity.KV_REL_TOL}},
+                   "checks": parity.RECORDS}, fh, indent=1)

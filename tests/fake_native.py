@@ -168,6 +168,9 @@ class FakeLiveTask:
                 self.state = DONE
         return SimpleNamespace(state=self.state, cursor=self.cursor, generation=0)
 
+    def max_entry_s(self):
+        return self.ctx.entry_s
+
     def destroy(self):
         self.destroyed = True
 

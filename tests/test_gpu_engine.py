@@ -9,6 +9,7 @@ import os
 import numpy as np
 import pytest
 
+import parity as P
 from oracle import forward as F
 
 pytestmark = pytest.mark.gpu
@@ -44,9 +45,7 @@ def test_config1_trace_parity(golden_dir):
     reqs = sorted(trace.requests, key=lambda r: r.num_tokens)[:6]
     for r in reqs:
         ol = F.forward_logits(shape, w, [tok(r)])[0]
-        g = b.logits[r.id]
-        e = np.abs(g - ol).max() / np.abs(ol).max()
-        assert e <= 0.03, (r.id, e)
+        P.logits(f"tiny config-1 run request {r.id} ({r.num_tokens} tokens)", b.logits[r.id], ol)
     assert ctx.free_pages() == 4096  # every task released its KV pages
     ctx.close()
 

@@ -1,19 +1,18 @@
 """GPU parity: the full preemptible forward pass through the C ABI vs the CPU fp32 oracle.
 
-Tolerance (bf16 path vs fp32 oracle; stated per BASELINE north_star): logits max-abs error
-<= LOGIT_ATOL_FRAC * max|logit| and KV max-abs error <= KV_ATOL_FRAC * max|kv|. GPU-vs-GPU
-comparisons (preempted vs straight, batched vs alone, chunked KV reuse) are bit-exact.
+Tolerance (bf16 path vs fp32 oracle; stated per BASELINE north_star, tests/parity.py): logits
+max-abs error <= 3% of max|logit| and relative L2 error <= 2%; KV max-abs <= 2% of max|kv| and
+relative L2 <= 1%. Both error kinds are printed and recorded for every comparison. GPU-vs-GPU
+comparisons (preempted vs straight, repeated runs) are bit-exact.
 """
 
 import numpy as np
 import pytest
 
+import parity as P
 from oracle import forward as F
 
 pytestmark = pytest.mark.gpu
-
-LOGIT_ATOL_FRAC = 0.03
-KV_ATOL_FRAC = 0.02
 
 
 @pytest.fixture(scope="module")
@@ -48,10 +47,7 @@ def test_golden_hf_logits(tiny, golden_dir):
     g = np.load(f"{golden_dir}/tiny_hf_logits.npz")
     tokens = F.make_tokens(list(g["lens"]), shape.vocab, int(g["seed"]))
     t = run_straight(ctx, tokens)
-    lg = t.logits()
-    e = rel_err(lg, g["logits"])
-    print("tiny GPU vs HF golden: max-abs/max", e)
-    assert e <= LOGIT_ATOL_FRAC
+    P.logits("tiny vs HF golden", t.logits(), g["logits"])
     t.destroy()
 
 
@@ -63,16 +59,13 @@ def test_logits_and_kv_vs_oracle(tiny, lens, chunk):
     ot = F.OracleTask(shape, w, tokens, chunk)
     ot.run_all()
     t = run_straight(ctx, tokens, chunk)
-    lg = t.logits()
-    e = rel_err(lg, ot.logits)
-    print(f"lens={lens} chunk={chunk}: logits rel err {e:.4g}")
-    assert e <= LOGIT_ATOL_FRAC
+    name = f"tiny lens={lens} chunk={chunk}"
+    P.logits(name, t.logits(), ot.logits)
     for r in range(len(lens)):
         for layer in (0, shape.num_layers - 1):
             k, v = t.read_kv(r, layer)
-            ek = rel_err(k, ot.k_cache[r][layer])
-            ev = rel_err(v, ot.v_cache[r][layer])
-            assert ek <= KV_ATOL_FRAC and ev <= KV_ATOL_FRAC, (r, layer, ek, ev)
+            P.kv(f"{name} K[{r}][{layer}]", k, ot.k_cache[r][layer])
+            P.kv(f"{name} V[{r}][{layer}]", v, ot.v_cache[r][layer])
     t.destroy()
 
 
@@ -154,15 +147,14 @@ def test_qwen_variants_vs_hf_and_oracle(golden_dir, name):
     t = run_straight(ctx, tokens, 96)
     lg = t.logits()
     assert lg.shape == (len(tokens), 8000)
-    e = rel_err(lg, g["logits"])
-    print(f"{name} GPU vs HF: {e:.4g}")
-    assert e <= LOGIT_ATOL_FRAC
+    P.logits(f"{name} vs HF golden", lg, g["logits"])
     ot = F.OracleTask(shape, w, tokens, 96)
     ot.run_all()
+    P.logits(f"{name} vs oracle", lg, ot.logits)
     for r in range(len(tokens)):
         k, v = t.read_kv(r, 1)
-        assert rel_err(k, ot.k_cache[r][1]) <= KV_ATOL_FRAC
-        assert rel_err(v, ot.v_cache[r][1]) <= KV_ATOL_FRAC
+        P.kv(f"{name} K[{r}][1]", k, ot.k_cache[r][1])
+        P.kv(f"{name} V[{r}][1]", v, ot.v_cache[r][1])
     t.destroy()
     ctx.close()
 
@@ -185,10 +177,11 @@ def test_forced_gemm_tiling_vs_oracle(tiny, policy):
         t.destroy()
     finally:
         ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
-    assert rel_err(lg, ot.logits) <= LOGIT_ATOL_FRAC
+    name = f"tiny gemm policy {policy}"
+    P.logits(name, lg, ot.logits)
     for r, (k, v) in enumerate(kv):
-        assert rel_err(k, ot.k_cache[r][shape.num_layers - 1]) <= KV_ATOL_FRAC
-        assert rel_err(v, ot.v_cache[r][shape.num_layers - 1]) <= KV_ATOL_FRAC
+        P.kv(f"{name} K[{r}]", k, ot.k_cache[r][shape.num_layers - 1])
+        P.kv(f"{name} V[{r}]", v, ot.v_cache[r][shape.num_layers - 1])
 
 
 def test_page_pool_exhaustion_is_clean():

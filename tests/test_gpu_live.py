@@ -72,3 +72,59 @@ def test_live_preemption_llama_shape():
     print("live llama4L:", res.commands, ps.slo_attainment(res.outcomes), bl)
     assert bl["max_s"] < 0.02  # one operator at 16K tokens is a few ms on a B200
     ctx.close()
+
+
+def test_live_replay_500_requests_llama3_8b():
+    """SURVEY.md §7 hard part 5 on the B200: a >= 500-request live run of the config-2 trace
+    (Llama-3-8B shape, S-EDF + operator preemption, B200-calibrated cost model) logs every
+    scheduling round; replaying the log through a FRESH reference SchedulerState /
+    schedule_round (scheduler.py:175-245) reproduces every command, the deferral protocol
+    (engine.py:419-502) holds, and every signal -> ACK is bounded by the preempted task's
+    longest executed entry (device stamps) plus host observation slack
+    (test_properties.py:90-94: blocking <= max_entry_s + c_check)."""
+    from paper_2602_16603_b200.calibrate import fit_cost_params
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.engine import synthetic_tokens
+    from paper_2602_16603_b200.live import replay_rounds, run_live
+    from paper_2602_16603_b200.native import PrefillContext
+
+    ps = refsim_or_skip()
+    import bench
+
+    shape = SHAPES["llama3-8b"]
+    ctx = PrefillContext(shape, kv_pages=3000, max_pos=40000)
+    ctx.init_random(0)
+    # B200 calibration (calibrate.py) from straight runs of the bench step's request lengths
+    ctx.profile(True)
+    ctx.drain_profile()
+    for i, r in enumerate(bench.step_requests(1, 0)):
+        t = ctx.create_task([np.random.default_rng(i).integers(0, shape.vocab, r.num_tokens)
+                             .astype(np.int32)])
+        t.begin_segment(0)
+        t.enqueue(0, t.n_entries)
+        ctx.sync()
+        t.destroy()
+    params = fit_cost_params(ctx.drain_profile(), shape.num_layers)
+    ctx.profile(False)
+    classes = [ps.TaskClass(*c) for c in bench.CONFIG2_CLASSES]
+    trace = ps.generate_trace(classes, 40.0, 13.0, 7)
+    assert len(trace) >= 500
+    pc = ps.PolicyConfig()
+    rounds: list = []
+    res = run_live(trace, pc, params, ctx, synthetic_tokens(5000, shape.vocab),
+                   max_wall_s=180, round_log=rounds)
+    rep = replay_rounds(trace, pc, params, rounds)  # raises on the first mismatch
+    assert rep["rounds"] == res.rounds == len(trace) + len(res.tasks)
+    assert rep["acks"] == res.commands["preempt"] >= 10
+    assert sorted(o.id for o in res.outcomes) == sorted(r.id for r in trace.requests)
+    max_entry = {r["done"]: r["max_entry_s"] for r in rounds if "done" in r}
+    slack = 2e-3  # host observation: one live-loop iteration (a scheduling round, a submit)
+    over = [(ack - sig, max_entry[tid]) for sig, ack, tid in res.blocking_log
+            if ack - sig > max_entry[tid] + slack]
+    bl = ps.blocking_stats(res.blocking_log)
+    print(f"live replay: {len(trace)} requests, {rep}, commands {res.commands}, attainment "
+          f"{ps.slo_attainment(res.outcomes):.3f}, blocking p99 {bl['p99_s'] * 1e3:.3f} ms, "
+          f"max {bl['max_s'] * 1e3:.3f} ms, longest entry {max(max_entry.values()) * 1e3:.3f} ms")
+    assert not over, over[:5]
+    assert ctx.free_pages() == 3000
+    ctx.close()

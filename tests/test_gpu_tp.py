@@ -17,6 +17,7 @@ import json
 import numpy as np
 import pytest
 
+import parity as P
 from oracle import forward as F
 
 pytestmark = pytest.mark.gpu
@@ -67,14 +68,13 @@ def test_tp_logits_kv_vs_oracle(weights, tp, lens, chunk):
     per_rank = t.rank_logits()
     for r in range(1, tp):  # replicated residual stream => identical logits on every rank
         assert np.array_equal(per_rank[r], per_rank[0]), r
-    e = rel_err(per_rank[0], ot.logits)
-    print(f"tp={tp} lens={lens} chunk={chunk}: logits rel err {e:.4g}")
-    assert e <= LOGIT_ATOL_FRAC
+    name = f"{NAME} tp={tp} lens={lens} chunk={chunk}"
+    P.logits(name, per_rank[0], ot.logits)
     for r in range(len(lens)):
         for layer in (0, shape.num_layers - 1):
             k, v = t.read_kv(r, layer)  # heads gathered rank-major = the model's head order
-            assert rel_err(k, ot.k_cache[r][layer]) <= KV_ATOL_FRAC
-            assert rel_err(v, ot.v_cache[r][layer]) <= KV_ATOL_FRAC
+            P.kv(f"{name} K[{r}][{layer}]", k, ot.k_cache[r][layer])
+            P.kv(f"{name} V[{r}][{layer}]", v, ot.v_cache[r][layer])
     cnt = g.tp_counters()
     assert len({(c["exchanges"], c["boundaries"]) for c in cnt}) == 1, cnt
     n_chunks = t.info()["n_chunks"]
@@ -199,7 +199,7 @@ def test_tp_reference_run_config1(golden_dir):
         assert dev_cursor == ref_cursor and state == 2
     r = min(trace.requests, key=lambda r: r.num_tokens)
     ol = F.forward_logits(shape, w, [tok(r)])[0]
-    assert rel_err(b.logits[r.id], ol) <= LOGIT_ATOL_FRAC
+    P.logits(f"{NAME} tp=2 config-1 run request {r.id}", b.logits[r.id], ol)
     g.close()
 
 
