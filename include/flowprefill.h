@@ -277,6 +277,11 @@ int fp_op_attn_prefill(fp_ctx* ctx, const void* q, const void* k, const void* v,
  * auto, S >= 1 forces S K-slices on the partial-wave tiles (clamped so the split units fit one
  * round of the persistent grid). */
 int fp_ctx_set_gemm_policy(fp_ctx* ctx, int32_t pair, int32_t splits);
+/* Batch-invariant numerics (also FP_BATCH_INVARIANT=1 at fp_ctx_create): no split-K and no
+ * stream-K, so each output element is one in-order accumulation over K whatever the launch's
+ * M, and a request's logits / KV are bit-identical alone or in any batch (SURVEY.md §7 hard
+ * part 7). Off by default: split-K is what makes short requests fast. */
+int fp_ctx_set_batch_invariant(fp_ctx* ctx, int32_t on);
 /* Diagnostics: with FP_GEMM_STAMPS=1 in the environment at fp_ctx_create, every fp_op_gemm
  * launch records per-CTA phase stamps (%globaltimer ns, 16 slots per CTA: entry, prologue done,
  * boundary check done, first TMA, first MMA, last accumulator commit, epilogue start, partial

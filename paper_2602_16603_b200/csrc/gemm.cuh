@@ -171,8 +171,8 @@ DEVI void split_barrier(int* ctr, int n) {
 struct GmemSum {
   const float4* ws_tile;
   int S;
+  template <int ILP = 4>
   DEVI void get(int r, int colA, int colB, float* v) const {
-    constexpr int ILP = 4;
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = 0.f;
     const float4* sa = ws_tile + (long long)(colA / 4) * kGemmBM + r;
@@ -311,7 +311,7 @@ DEVI void tp_fold_tile(const GemmParams& p, const TpDev* tp, int slot, unsigned 
 // EPI_RESID writes the row's sum of squares (8 chunk sums in chunk order) to ssq_out; the Qwen3
 // q/k-norm sums a head's 4 items in quarter order.
 template <int EPI>
-__device__ __noinline__ void split_item_epilogue(const GemmParams& p, const GmemSum& sum,
+__device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const GmemSum& sum,
                                                  bool valid, int m, int r, int g, int n0,
                                                  int nb) {
   constexpr int BN = 256;
@@ -393,7 +393,7 @@ __device__ __noinline__ void split_item_epilogue(const GemmParams& p, const Gmem
     const float* hn = is_v ? nullptr : (is_q ? p.q_norm : p.k_norm);
     float ss = 0.f;
     if (live) {
-      sum.get(r, hh * 128 + q * 16, hh * 128 + 64 + q * 16, v);
+      sum.get<2>(r, hh * 128 + q * 16, hh * 128 + 64 + q * 16, v);  // ILP 2: register budget
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= rs;
       if (bias) {
@@ -868,10 +868,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       };
 
       if constexpr (EPI == EPI_RESID) {
-        // residual row segment prefetched into registers while the MMA runs
-        uint4 hres[BN / 8];
+        // residual row segment prefetched into registers while the MMA runs (MODE 1 loads it
+        // per 32-column chunk instead: the split path's registers leave no room for 128 more)
+        constexpr bool kPrefetch = MODE != 1;
+        uint4 hres[kPrefetch ? BN / 8 : 1];
         __nv_bfloat16* hrow = p.resid + (long long)m * p.ldr + n0;
-        if (live) {
+        if (kPrefetch && live) {
 #pragma unroll
           for (int i = 0; i < BN / 8; ++i) hres[i] = ld_global_v4(hrow + 8 * i);
         }
@@ -886,7 +888,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (live) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const uint4 h = hres[c * 4 + i];
+              const uint4 h = kPrefetch ? hres[(c * 4 + i) % (kPrefetch ? BN / 8 : 1)]
+                                        : ld_global_v4(hrow + c * 32 + 8 * i);
               const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -959,9 +962,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int pos = live ? p.pos[m] : 0;
         const int page = live ? p.tok_page[m] : 0;
         // (cos, sin) of the row's position for the 64 rotation pairs, prefetched during the MMA
-        float4 cs[32];
+        // (MODE 1 reads them per half at use: no room for 128 prefetched registers there)
+        constexpr bool kPrefetch = MODE != 1;
+        float4 cs[kPrefetch ? 32 : 1];
         const bool rot = n0 < p.q_cols + p.kv_cols;  // tile holds q/k heads (v heads unrotated)
-        if (live && rot) {
+        const float4* cs_src = reinterpret_cast<const float4*>(p.rope + (long long)pos * 64);
+        if (kPrefetch && live && rot) {
           const float4* src = reinterpret_cast<const float4*>(p.rope + (long long)pos * 64);
 #pragma unroll
           for (int i = 0; i < 32; ++i) cs[i] = __ldg(src + i);
@@ -1027,7 +1033,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if (!is_v) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                  const float4 t4 = cs[half * 16 + i];  // (cos, sin) of columns 2i, 2i+1
+                  // (cos, sin) of columns 2i, 2i+1
+                  const float4 t4 = kPrefetch ? cs[(half * 16 + i) % (kPrefetch ? 32 : 1)]
+                                              : __ldg(cs_src + half * 16 + i);
                   const float u1 = a[2 * i], u2 = b[2 * i];
                   const float w1 = a[2 * i + 1], w2 = b[2 * i + 1];
                   a[2 * i] = u1 * t4.x - u2 * t4.y;

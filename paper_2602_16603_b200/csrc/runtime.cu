@@ -237,6 +237,11 @@ struct fp_ctx {
   // power-capped B200 (the idle SMs of a partial wave cost little energy; the partial round
   // trips add traffic). Policy 3 forces it in the parity tests.
   bool use_streamk = true;
+  // Batch-invariant numerics (FP_BATCH_INVARIANT=1 / fp_ctx_set_batch_invariant): no split-K
+  // and no stream-K, so every output element is ONE in-order TMEM accumulation over K whatever
+  // the launch's M -- a request's logits and KV are then bit-identical alone or in any batch
+  // (SURVEY.md §7 hard part 7). Costs the short-request speed-up of split-K.
+  bool batch_invariant = false;
   int* sk_flags = nullptr;  // stream-K partial flags [num_sms]
   int sk_epoch = 0;         // per stream-K launch (flags compare against it: no reset)
 };
@@ -383,6 +388,10 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
     choose_splits(tiles, p.K / kGemmBK, slots, &p.full_tiles, &p.splits, split_tail_ok(EPI, p.K),
                   split_overhead(EPI));
   if (p.xchg) {  // TP exchange GEMMs publish / fold their partials per tile: never split
+    p.splits = 1;
+    p.full_tiles = tiles;
+  }
+  if (c->batch_invariant) {
     p.splits = 1;
     p.full_tiles = tiles;
   }
@@ -559,7 +568,8 @@ static double plan_cost_tiled(const fp_ctx* c, int epi, int M, int N, int K) {
 template <int EPI>
 static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
                         const GemmParams& p, cudaStream_t st) {
-  if (!p.xchg && (c->force_pair == 3 || (c->use_streamk && c->force_pair < 0 && c->force_splits == 0))) {
+  if (!p.xchg && !c->batch_invariant &&
+      (c->force_pair == 3 || (c->use_streamk && c->force_pair < 0 && c->force_splits == 0))) {
     const SkPlan pl = plan_streamk(c, p.M, p.N, p.K);
     if (pl.grid >= 2 &&
         (c->force_pair == 3 || pl.cost < 0.92 * plan_cost_tiled(c, EPI, p.M, p.N, p.K))) {
@@ -1108,6 +1118,7 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
     if (const char* e = getenv("FP_PAIR_GEMM")) c->use_pair_gemm = atoi(e) != 0;
     if (const char* e = getenv("FP_NARROW")) c->use_narrow = atoi(e) != 0;
     if (const char* e = getenv("FP_STREAMK")) c->use_streamk = atoi(e) != 0;
+    if (const char* e = getenv("FP_BATCH_INVARIANT")) c->batch_invariant = atoi(e) != 0;
     if (const char* e = getenv("FP_RASTER_ALL_MB")) g_raster_all_mb = atoi(e);
     if (const char* e = getenv("FP_SK_FIX_SCALE")) g_sk_fix_scale = atof(e);
     if (const char* e = getenv("FP_SPLIT_OV_SCALE")) g_split_ov_scale = atof(e);
@@ -1248,6 +1259,11 @@ int fp_ctx_set_gemm_policy(fp_ctx* c, int32_t pair, int32_t splits) {
   REQ(c && pair >= -1 && pair <= 3 && splits >= 0 && splits <= 32, "bad gemm policy");
   c->force_pair = pair;
   c->force_splits = splits;
+  return FP_OK;
+}
+int fp_ctx_set_batch_invariant(fp_ctx* c, int32_t on) {
+  REQ(c, "null ctx");
+  c->batch_invariant = on != 0;
   return FP_OK;
 }
 int fp_sync(fp_ctx* c) {

@@ -159,6 +159,11 @@ class PrefillContext:
     def set_window(self, entries: int) -> None:
         _lib.check(self.lib.fp_ctx_set_window(self.h, entries), "fp_ctx_set_window")
 
+    def set_batch_invariant(self, on: bool) -> None:
+        """No split-K / stream-K: a request's results are bit-identical in any batch."""
+        _lib.check(self.lib.fp_ctx_set_batch_invariant(self.h, 1 if on else 0),
+                   "fp_ctx_set_batch_invariant")
+
     # -- live profiling -------------------------------------------------------------
     def profile(self, on: bool) -> None:
         _lib.check(self.lib.fp_prof_enable(self.h, 1 if on else 0), "fp_prof_enable")

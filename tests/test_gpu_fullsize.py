@@ -111,6 +111,29 @@ def test_longest_trace_request_and_ragged_batch(ctx):
         a.destroy()
 
 
+def test_batch_invariant_mode_full_size(ctx):
+    """Llama-3-8B, 32 layers, batch-invariant mode (no split-K / stream-K): each request of a
+    ragged batch gives bit-identical logits and KV alone and batched (SURVEY.md §7 hard
+    part 7) -- the tile shape (pair / single / narrow) a launch picks from its M does not
+    change any bits, only the K-reduction split would."""
+    lens = [1, 127, 129, 700, 4097]
+    tokens = [toks(n, 20 + n) for n in lens]
+    ctx.set_batch_invariant(True)
+    try:
+        b = run(ctx, tokens)
+        lb = b.logits()
+        kb = [b.read_kv(i, 31) for i in range(len(lens))]
+        b.destroy()
+        for i, tk in enumerate(tokens):
+            a = run(ctx, [tk])
+            assert np.array_equal(a.logits()[0], lb[i]), lens[i]
+            k, v = a.read_kv(0, 31)
+            assert np.array_equal(k, kb[i][0]) and np.array_equal(v, kb[i][1]), lens[i]
+            a.destroy()
+    finally:
+        ctx.set_batch_invariant(False)
+
+
 def test_chunked_matches_unchunked(ctx):
     tokens = [toks(9000, 3), toks(700, 4)]
     u = run(ctx, tokens)
