@@ -571,7 +571,7 @@ def preemption_latency(ctx, shape, rank: int, n_signals: int = 40, length: int =
 
 def live_run(ctx, shape, params, pc, rate, duration):
     from paper_2602_16603_b200 import refsim
-    from paper_2602_16603_b200.live import run_live
+    from paper_2602_16603_b200.live import replay_rounds, run_live
 
     ps = refsim.load()
     base = config2_trace(rate=20.0, duration=duration * rate / 20.0)
@@ -581,8 +581,18 @@ def live_run(ctx, shape, params, pc, rate, duration):
         return np.random.default_rng(5000 + r.id).integers(0, shape.vocab, r.num_tokens).astype(np.int32)
 
     t0 = time.perf_counter()
-    res = run_live(trace, pc, params, ctx, tok, max_wall_s=10 * duration + 60)
+    rounds: list = []
+    res = run_live(trace, pc, params, ctx, tok, max_wall_s=10 * duration + 60, round_log=rounds)
+    wall = time.perf_counter() - t0
     bl = ps.blocking_stats(res.blocking_log)
+    # wall-clock scheduling parity: every round replayed through a fresh reference scheduler
+    try:
+        rep = replay_rounds(trace, pc, params, rounds)
+        replay = {"rounds": rep["rounds"], "commands": rep["commands"], "mismatches": 0}
+    except AssertionError as e:
+        replay = {"mismatch": str(e)[:300]}
+    max_entry = {r["done"]: r["max_entry_s"] for r in rounds if "done" in r}
+    over = sum(1 for sig, ack, tid in res.blocking_log if ack - sig > max_entry.get(tid, 0.0) + 2e-3)
     return {
         "rate_req_s": round(rate, 3),
         "requests": len(trace),
@@ -593,7 +603,9 @@ def live_run(ctx, shape, params, pc, rate, duration):
         "rounds": res.rounds,
         "p99_blocking_ms": None if bl["p99_s"] is None else round(bl["p99_s"] * 1e3, 3),
         "max_blocking_ms": None if bl["max_s"] is None else round(bl["max_s"] * 1e3, 3),
-        "wall_s": round(time.perf_counter() - t0, 2),
+        "wall_s": round(wall, 2),
+        "replay": replay,
+        "blocking_over_max_entry_plus_2ms": over,
     }
 
 

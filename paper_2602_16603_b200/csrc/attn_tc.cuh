@@ -53,8 +53,24 @@ struct AttnTcParams {
   int kv_rows_per_page;           // 2 * n_kv_heads * 128 rows per page (one layer)
   float scale_log2;               // log2(e) / sqrt(128)
   int* sched;                     // [2] work counter, finished CTAs (zero between launches)
+  unsigned long long* dbg;        // -DFP_GEMM_STAMPS builds: clock64 phase stamps (see ATTN_STAMP)
   Guard guard;
 };
+
+// Diagnostic builds only (-DFP_GEMM_STAMPS): SM clock64 at the phases of the first work item of
+// CTAs 0..15, KV tiles 0..63: [cta][tile][8] = softmax h0 sees S, h0 arrives P, h1 sees S,
+// h1 arrives P, MMA issues PV0, MMA issued QK0(j+1), MMA issues PV1, MMA issued QK1(j+1).
+#ifdef FP_GEMM_STAMPS
+#define ATTN_STAMP(it, j, k)                                                              \
+  do {                                                                                    \
+    if (p.dbg && (it) == 0 && blockIdx.x < 16 && (j) < 64)                                 \
+      p.dbg[((int)blockIdx.x * 64 + (j)) * 8 + (k)] = (unsigned long long)clock64();       \
+  } while (0)
+#else
+#define ATTN_STAMP(it, j, k) \
+  do {                       \
+  } while (0)
+#endif
 
 namespace tcattn {
 constexpr int THREADS = 320;
@@ -309,6 +325,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         mbar_wait(&p_full[0], tph);
         if (j == 0) mbar_wait(&o_empty[0], (it & 1) ^ 1);  // previous item's O0 drained
         tc_fence_after();
+        if (lane == 0) ATTN_STAMP(it, j, 4);
         if (lane == 0) issue_pv(0, vsq, j > 0);
         __syncwarp();
         if (!last) {
@@ -317,18 +334,21 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           if (lane == 0) {
             issue_qk(0, ksq);
             tc_commit(&s_full[0]);
+            ATTN_STAMP(it, j, 5);
           }
           __syncwarp();
         }
         mbar_wait(&p_full[1], tph);
         if (j == 0) mbar_wait(&o_empty[1], (it & 1) ^ 1);
         tc_fence_after();
+        if (lane == 0) ATTN_STAMP(it, j, 6);
         if (lane == 0) {
           issue_pv(1, vsq, j > 0);
           tc_commit(&kv_empty[slot_of(vsq)]);
           if (!last) {
             issue_qk(1, ksq);
             tc_commit(&s_full[1]);
+            ATTN_STAMP(it, j, 7);
             tc_commit(&kv_empty[slot_of(ksq)]);
             if (j + 1 == n_tiles - 1) tc_commit(q_empty);  // last QK^T of the item issued
           }
@@ -368,6 +388,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       for (int j = 0; j < a.n_tiles; ++j) {
         mbar_wait(&s_full[h], (tc + j) & 1);
         tc_fence_after();
+        if (row == 0) ATTN_STAMP(it, j, 2 * h);
         uint32_t su[4][32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, su[c]);
@@ -433,6 +454,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[h]);
+        if (row == 0) ATTN_STAMP(it, j, 2 * h + 1);
       }
       // epilogue: O / l -> bf16 -> HBM, then release O for the next item's first P*V
       mbar_wait(o_full, it & 1);

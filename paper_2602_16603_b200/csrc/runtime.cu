@@ -862,6 +862,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
     a.kv_rows_per_page = 2 * c->hkv * c->page_size;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)m.head_dim);
     a.sched = c->attn_sched;
+    a.dbg = c->gemm_dbg;
     a.guard = g;
     if (a.n_items > 0) {
       ProfScope ps(c, st, FP_K_ATTN, layer, M, ch.attn_flops, 0.0);
@@ -2203,6 +2204,7 @@ int fp_op_attn_prefill(fp_ctx* c, const void* q, const void* k, const void* v, v
     a.kv_rows_per_page = 2 * H * PS;
     a.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
     a.sched = c->attn_sched;
+    a.dbg = c->gemm_dbg;
     launch_attn(c, tq, c->tm_kv, a, st);
   }
   CK(cudaFreeAsync(meta, st));

@@ -66,6 +66,46 @@ def sdpa(n: int, reps: int, backend) -> float:
     return float(np.median(ts))
 
 
+def fa4(n: int, reps: int) -> float:
+    """FlashAttention-4 (CuTe DSL sm100 kernel shipped with vllm): [b, s, h, d] layout."""
+    import torch
+    from vllm.vllm_flash_attn.cute.interface import flash_attn_func
+
+    q = torch.randn(1, n, 32, 128, device="cuda", dtype=torch.bfloat16)
+    k = torch.randn(1, n, 8, 128, device="cuda", dtype=torch.bfloat16)
+    v = torch.randn(1, n, 8, 128, device="cuda", dtype=torch.bfloat16)
+    f = lambda: flash_attn_func(q, k, v, causal=True)  # noqa: E731
+    return _time(f, reps)
+
+
+def flashinfer_prefill(n: int, reps: int) -> float:
+    import flashinfer
+    import torch
+
+    q = torch.randn(n, 32, 128, device="cuda", dtype=torch.bfloat16)
+    k = torch.randn(n, 8, 128, device="cuda", dtype=torch.bfloat16)
+    v = torch.randn(n, 8, 128, device="cuda", dtype=torch.bfloat16)
+    f = lambda: flashinfer.single_prefill_with_kv_cache(q, k, v, causal=True)  # noqa: E731
+    return _time(f, reps)
+
+
+def _time(f, reps):
+    import torch
+
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        f()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--len", type=int, action="append", default=[])
@@ -83,6 +123,11 @@ def main():
                 rows.append((name, sdpa(n, a.reps, be)))
             except Exception as e:  # backend unavailable for this shape / arch
                 print(f"n={n} {name}: unavailable ({str(e).splitlines()[0][:100]})")
+        for name, fn in (("flash-attn 4 (cute dsl)", fa4), ("flashinfer prefill", flashinfer_prefill)):
+            try:
+                rows.append((name, fn(n, a.reps)))
+            except Exception as e:
+                print(f"n={n} {name}: unavailable ({str(e).splitlines()[0][:100] if str(e) else repr(e)})")
         for name, ms in rows:
             print(f"n={n:6d} {name:26s} {ms * 1e3:9.1f} us  {flops / ms / 1e9:8.1f} TFLOP/s")
 
