@@ -701,6 +701,149 @@ def calibrated_goodput(prof, shape, args, n_instances: int = 1):
     return out
 
 
+def run_tp(args):
+    """Config 4: Qwen2.5-32B shape, tensor parallel over `--tp N` GPUs, one
+    process per GPU. Every rank runs the SAME requests on its Megatron shard; the o_proj /
+    down_proj GEMMs are the fused exchange kernels (each tile's partial flagged to the peers and
+    folded over peer memory while the next tile's MMAs run), and rank 0 decides every boundary
+    for all ranks. value = the step's tokens (counted once, not per rank) / the slowest rank's
+    device time: strong scaling. The exchange share per rank is the o_proj + down_proj kernel
+    time from the profiled steps (the all-reduce lives inside those kernels)."""
+    import torch
+
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext, connect_tp_dist
+
+    ws, rank, local = dist_env()
+    if ws != args.tp:
+        raise SystemExit(f"--tp {args.tp} needs {args.tp} ranks (WORLD_SIZE={ws})")
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shape = SHAPES["qwen2.5-32b"]
+    reqs = step_requests(1, 0)[: args.tp_requests]
+    lens = [r.num_tokens for r in reqs]
+    tokens = [np.random.default_rng(1000 + r.id).integers(0, shape.vocab, r.num_tokens)
+              .astype(np.int32) for r in reqs]
+    step_tokens = int(sum(lens))
+    pages = sum((n + 127) // 128 for n in lens)
+    ctx = PrefillContext(shape, device=local, kv_pages=2 * pages + 64, page_size=128,
+                         max_pos=40000, tp_rank=rank, tp_size=ws)
+    if ws > 1:
+        connect_tp_dist(ctx, max(lens))
+    ctx.init_random(seed=0)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=local)
+    tasks = [ctx.create_task([t], None, "operator", i) for i, t in enumerate(tokens)]
+
+    def run_step():
+        for t in tasks:
+            t.begin_segment(0)
+            t.enqueue(0, t.n_entries)
+
+    def reduce(x: float, op) -> float:
+        if dist is None:
+            return x
+        v = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(v, op=op)
+        return float(v.item())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 1)):
+        run_step()
+    ctx.sync()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launch_count()
+    barrier()
+    torch.cuda.synchronize(local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        run_step()
+    e1.record(stream)
+    ctx.sync()
+    torch.cuda.synchronize(local)
+    barrier()
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop()
+    ms_max = reduce(e0.elapsed_time(e1), dist.ReduceOp.MAX if dist else None)
+    value = step_tokens * args.steps / (ms_max / 1e3)
+    # per-kernel profile (one step): exchange share and the dominant GEMM's rate
+    ctx.profile(True)
+    ctx.drain_profile()
+    run_step()
+    prof = ctx.drain_profile()
+    ctx.profile(False)
+    tot = sum(r["ms"] for r in prof)
+    xch = sum(r["ms"] for r in prof if r["kind"] in ("o_gemm", "down_gemm", "allreduce"))
+    gu = [r for r in prof if r["kind"] == "gate_up_gemm"]
+    gu_tf = sum(r["flops"] for r in gu) / (sum(r["ms"] for r in gu) * 1e-3) / 1e12 if gu else 0.0
+    share = reduce(xch / tot if tot else 0.0, dist.ReduceOp.MAX if dist else None)
+    # e2e: host token ids -> host logits through the public API, copies inside the region
+    barrier()
+    ctx.sync()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        live = []
+        for i, t in enumerate(tokens):
+            task = ctx.create_task([t], None, "operator", 10_000 + i)
+            h2d += task.info()["upload_bytes"]
+            task.begin_segment(0)
+            task.enqueue(0, task.n_entries)
+            live.append(task)
+        for task in live:
+            d2h += task.logits().nbytes
+            task.destroy()
+    ctx.sync()
+    e2e_s = reduce(time.perf_counter() - t0, dist.ReduceOp.MAX if dist else None)
+    for t in tasks:
+        t.destroy()
+    if rank == 0:
+        peaks, peak_kind = measured_peaks()
+        peak = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
+        line = {
+            "metric": "prefill_tokens_per_s",
+            "value": value,
+            "unit": "tok/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (random-init weights, seeded token ids, config-2 trace lengths)",
+            "config": {"workload": f"qwen2.5-32b prefill, tensor parallel TP={ws}, "
+                                   f"{len(reqs)} requests/step of the config-2 trace",
+                       "model": "qwen2.5-32b", "tokens_per_step": step_tokens,
+                       "request_lens": lens, "parallelism": f"tp{ws}",
+                       "l2": "inputs larger than L2 (weights streamed per step)"},
+            "roofline": {"bound": "tensor", "kernel": "gate_up_proj GEMM + SwiGLU (per rank)",
+                         "achieved": round(gu_tf, 1), "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(gu_tf / peak, 4) if peak else None, "traffic": None,
+                         "peak_source": peak_kind},
+            "exchange_share_per_rank": round(share, 4),
+            "e2e": {"value": step_tokens * args.steps / e2e_s, "unit": "tok/s",
+                    "h2d_bytes_per_step": int(h2d // args.steps),
+                    "d2h_bytes_per_step": int(d2h // args.steps)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -713,9 +856,16 @@ def main():
     ap.add_argument("--skip-live", action="store_true")
     ap.add_argument("--live-duration", type=float, default=10.0)
     ap.add_argument("--live-probes", type=int, default=3)
+    ap.add_argument("--tp", type=int, default=0,
+                    help="config 4: Qwen2.5-32B tensor parallel over this many GPUs (one rank each)")
+    ap.add_argument("--tp-requests", type=int, default=STEP_REQUESTS)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.tp:
+        if args.tp > 1 and "WORLD_SIZE" not in os.environ:
+            sys.exit(spawn_ranks(args.tp))
+        run_tp(args)
     elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
     else:

@@ -58,13 +58,15 @@ struct AttnTcParams {
 };
 
 // Diagnostic builds only (-DFP_GEMM_STAMPS): SM clock64 at the phases of the first work item of
-// CTAs 0..15, KV tiles 0..63: [cta][tile][8] = softmax h0 sees S, h0 arrives P, h1 sees S,
-// h1 arrives P, MMA issues PV0, MMA issued QK0(j+1), MMA issues PV1, MMA issued QK1(j+1).
+// CTAs 0..15, KV tiles 0..63: [cta][tile][24] = softmax h0 sees S, h0 arrives P, h1 sees S,
+// h1 arrives P, MMA issues PV0, MMA issued QK0(j+1), MMA issues PV1, MMA issued QK1(j+1), MMA
+// has K(j+1), -, then per head h: S in registers (10 + 4h), row max done (11 + 4h), P
+// computed (12 + 4h), row sum done (13 + 4h).
 #ifdef FP_GEMM_STAMPS
 #define ATTN_STAMP(it, j, k)                                                              \
   do {                                                                                    \
     if (p.dbg && (it) == 0 && blockIdx.x < 16 && (j) < 64)                                 \
-      p.dbg[((int)blockIdx.x * 64 + (j)) * 8 + (k)] = (unsigned long long)clock64();       \
+      p.dbg[((int)blockIdx.x * 64 + (j)) * 24 + (k)] = (unsigned long long)clock64();       \
   } while (0)
 #else
 #define ATTN_STAMP(it, j, k) \
@@ -331,6 +333,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         if (!last) {
           wait_tile(ksq);
           tc_fence_after();
+          if (lane == 0) ATTN_STAMP(it, j, 8);
           if (lane == 0) {
             issue_qk(0, ksq);
             tc_commit(&s_full[0]);
@@ -396,6 +399,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         float sr[128];
 #pragma unroll
         for (int i = 0; i < 128; ++i) sr[i] = __uint_as_float(su[i >> 5][i & 31]);
+        if (row == 0) ATTN_STAMP(it, j, 10 + 4 * h);
         const int kv0 = j * TILE;
         if (kv0 + TILE - 1 > a.it.q_pos0) {  // diagonal tile: causal mask
 #pragma unroll
@@ -406,6 +410,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
 #pragma unroll
         for (int i = 1; i < 128; ++i) mx = fmaxf(mx, sr[i]);
         const float m_new = fmaxf(m, mx * sc);  // scaled (log2) units
+        if (row == 0) ATTN_STAMP(it, j, 11 + 4 * h);
         if (j == 0) {
           m = m_new;
         } else {
@@ -429,7 +434,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           }
         }
         const float nm = (m == -INFINITY) ? 0.f : -m;
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
@@ -444,17 +448,27 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
               e.x = fast_exp2(x.x);
               e.y = fast_exp2(x.y);
             }
-            if (i & 2) acc1 = fadd2(acc1, e);
-            else acc0 = fadd2(acc0, e);
+            sr[c * 32 + i] = e.x;  // kept for the row sum, taken after P is released
+            sr[c * 32 + i + 1] = e.y;
             pk[i >> 1] = pack_bf16x2(e.x, e.y);
           }
           tmem_st16(tS + c * 16, pk);  // P (bf16 pairs) over the consumed S columns
         }
-        l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+        if (row == 0) ATTN_STAMP(it, j, 12 + 4 * h);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[h]);
         if (row == 0) ATTN_STAMP(it, j, 2 * h + 1);
+        // row sum off the P -> PV critical path (same pairing and order as before)
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 128; i += 2) {
+          const float2 e = make_float2(sr[i], sr[i + 1]);
+          if (i & 2) acc1 = fadd2(acc1, e);
+          else acc0 = fadd2(acc0, e);
+        }
+        l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+        if (row == 0) ATTN_STAMP(it, j, 13 + 4 * h);
       }
       // epilogue: O / l -> bf16 -> HBM, then release O for the next item's first P*V
       mbar_wait(o_full, it & 1);

@@ -439,6 +439,17 @@ class TPTask:
         for t in self.parts:
             t.begin_segment(first)
 
+    def start(self, first: int) -> None:
+        """The asynchronous launch worker (``fp_task_start``) drives ONE context. Ranks driven
+        in lock step from one process cannot each run a worker (a rank's exchange kernel would
+        wait for peers whose launches are queued behind it on the shared stream), so a
+        ``TPGroup`` runs the virtual-clock parity driver (``engine.run_on_gpu``) only; the
+        wall-clock driver runs tensor parallelism as one process per GPU, each rank a
+        ``PrefillContext`` with its own worker (``connect_tp_dist``)."""
+        raise NotImplementedError(
+            "TPGroup tasks run under the virtual-clock driver only; for the wall-clock driver "
+            "run one process per GPU (PrefillContext(tp_rank=..., tp_size=...) + connect_tp_dist)")
+
     def enqueue(self, first: int, last: int) -> None:
         n = self.group.tp_size
         ctxs = (C.c_void_p * n)(*[c.h.value for c in self.group.ranks])

@@ -267,3 +267,15 @@ def test_op_tp_allreduce(tp):
                 assert torch.equal(hs[r], ref), r
     finally:
         g.close()
+
+
+def test_tp_group_has_no_wall_clock_worker(weights):
+    """A lock-step TPGroup is parity-mode only: start() (the async worker the live driver
+    uses) fails loudly instead of deadlocking the ranks' exchange."""
+    shape, w = weights
+    g = make_group(2, w)
+    t = g.create_task(F.make_tokens([40], shape.vocab, 1))
+    with pytest.raises(NotImplementedError):
+        t.start(0)
+    t.destroy()
+    g.close()

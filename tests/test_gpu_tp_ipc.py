@@ -24,7 +24,7 @@ pytestmark = pytest.mark.gpu
 NAME = "tiny-qwen2-tp"
 
 
-def _rank_main(rank, size, port, q, fused=True):
+def _rank_main(rank, size, port, q, fused=True, distinct=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
@@ -36,7 +36,7 @@ def _rank_main(rank, size, port, q, fused=True):
 
         shape = F.SHAPES[NAME]
         w = F.make_weights(shape, 4321)
-        ctx = PrefillContext(SHAPES[NAME], device=0, kv_pages=64, max_pos=4096,
+        ctx = PrefillContext(SHAPES[NAME], device=rank if distinct else 0, kv_pages=64, max_pos=4096,
                              tp_rank=rank, tp_size=size)
         connect_tp_dist(ctx, 1024)
         ctx.load_weights(w)
@@ -76,11 +76,12 @@ def _rank_main(rank, size, port, q, fused=True):
         dist.destroy_process_group()
 
 
-def _run_group(fused):
+def _run_group(fused, distinct=False):
     size, port = 2, random.randint(20000, 40000)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank_main, args=(r, size, port, q, fused)) for r in range(size)]
+    procs = [ctx.Process(target=_rank_main, args=(r, size, port, q, fused, distinct))
+             for r in range(size)]
     for p in procs:
         p.start()
     try:
@@ -124,3 +125,23 @@ def test_tp2_fused_exchange_matches_two_kernel_exchange():
             assert np.abs(a - b).max() / np.abs(b).max() <= 0.01
         assert np.array_equal(fused[r][0], fused[r][3])  # fused: preemption changes no bits
         assert fused[r][4]["exchanges"] == split[r][4]["exchanges"]
+
+
+@pytest.mark.timeout(300)
+def test_tp2_two_devices_ipc():
+    """The deployment form of config 4 on real hardware: rank r on GPU r, the exchange blocks
+    mapped over CUDA IPC across devices (NVLink peer memory). Skipped on a 1-GPU box."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = _run_group(fused=True, distinct=True)
+    shape = F.SHAPES[NAME]
+    w = F.make_weights(shape, 4321)
+    ref = F.forward_logits(shape, w, F.make_tokens([300, 37], shape.vocab, 11))
+    s0, s1 = res[0][0], res[1][0]
+    assert np.array_equal(s0, s1)
+    P.logits(f"{NAME} tp=2 two devices (fused exchange)", s0, ref)
+    k = 5 * shape.num_layers // 2 + 1
+    assert res[0][1] == res[1][1] == (2, k)
+    assert np.array_equal(res[0][3], s0) and np.array_equal(res[1][3], s0)

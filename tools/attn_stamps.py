@@ -66,9 +66,10 @@ def main():
     _lib.check(c.lib.fp_debug_gemm_stamps(c.h, buf.ctypes.data, 4096))
     flops = 4 * hq * 128 * n * (n + 1) / 2
     print(f"len {n}: {ms * 1e3:.1f} us (incl. op overhead), {flops / ms / 1e9:.1f} TFLOP/s")
-    s = buf.reshape(-1)[: 16 * 64 * 8].reshape(16, 64, 8).astype(np.int64)
+    s = buf.reshape(-1)[: 16 * 64 * 24].reshape(16, 64, 24).astype(np.int64)
     names = ["h0 S seen", "h0 P out", "h1 S seen", "h1 P out", "PV0 issue", "QK0 issued",
-             "PV1 issue", "QK1 issued"]
+             "PV1 issue", "QK1 issued", "K(j+1) in", "-", "h0 S regs", "h0 max", "h0 P st",
+             "h0 sum", "h1 S regs", "h1 max", "h1 P st", "h1 sum"]
     for cta in range(2):
         t = s[cta]
         nt = int((t[:, 0] > 0).sum())
@@ -76,9 +77,19 @@ def main():
             continue
         t0 = t[0, 0]
         print(f"CTA {cta}: {nt} KV tiles (clock64 cycles relative to h0 S seen of tile 0)")
-        print("tile " + " ".join(f"{x:>11s}" for x in names))
+        print("tile " + " ".join(f"{x:>10s}" for x in names))
         for j in range(min(nt, 12)):
-            print(f"{j:4d} " + " ".join(f"{(x - t0) if x else 0:11d}" for x in t[j]))
+            print(f"{j:4d} " + " ".join(f"{(x - t0) if x else 0:10d}" for x in t[j, :18]))
+        mid = slice(1, nt - 1)
+        for h in (0, 1):
+            b = 10 + 4 * h
+            seen = t[mid, 2 * h]
+            print(f"  head {h} softmax phases (median cycles): S seen->regs "
+                  f"{np.median(t[mid, b] - seen):.0f}, ->max {np.median(t[mid, b + 1] - t[mid, b]):.0f}, "
+                  f"->P stored {np.median(t[mid, b + 2] - t[mid, b + 1]):.0f}, ->arrive "
+                  f"{np.median(t[mid, 2 * h + 1] - t[mid, b + 2]):.0f}, ->sum {np.median(t[mid, b + 3] - t[mid, 2 * h + 1]):.0f}")
+        print(f"  MMA: PV0 issue -> K(j+1) in {np.median(t[mid, 8] - t[mid, 4]):.0f}, K in -> QK0 issued "
+              f"{np.median(t[mid, 5] - t[mid, 8]):.0f}")
         sm0 = t[1:nt - 1, 1] - t[1:nt - 1, 0]  # softmax h0 latency (S seen -> P out)
         sm1 = t[1:nt - 1, 3] - t[1:nt - 1, 2]
         per = np.diff(t[1:nt - 1, 0])          # h0 period per tile
