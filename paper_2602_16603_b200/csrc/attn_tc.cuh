@@ -79,7 +79,10 @@ constexpr int THREADS = 320;
 constexpr int TILE = 128;
 constexpr int TILE_BYTES = 128 * 128 * 2;  // 32 KB: two 64-column swizzle atoms of 16 KB
 constexpr int ATOM_BYTES = 16384;
-constexpr int STAGES = 3;
+#ifndef FP_ATTN_STAGES
+#define FP_ATTN_STAGES 3
+#endif
+constexpr int STAGES = FP_ATTN_STAGES;
 constexpr int SMEM_BYTES = 1024 + 2 * TILE_BYTES + STAGES * TILE_BYTES + 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: rescale O only if max grows > 256x
 constexpr int SOFTMAX_WARPS = 8;
@@ -274,22 +277,26 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     uint32_t seq = 0;  // ring sequence number of the next K/V tile to consume
     auto slot_of = [&](uint32_t sq) { return (int)(sq % STAGES); };
     auto wait_tile = [&](uint32_t sq) { mbar_wait(&kv_full[slot_of(sq)], (sq / STAGES) & 1); };
+    // Descriptors are built once (Q) or once per group of 8 MMAs (K / V slot) and advanced by
+    // constant offsets: building one per MMA costs more issue time than an N = 128 MMA takes
+    // to execute (tools/probes/mma_rate.cu: 66 vs ~170 cycles per MMA).
+    const uint64_t qdesc[2] = {make_sdesc_sw128(smem_u32(sQ), 16, 1024),
+                               make_sdesc_sw128(smem_u32(sQ + TILE_BYTES), 16, 1024)};
     auto issue_qk = [&](int h, uint32_t ksq) {
-      const uint32_t kb = smem_u32(sKV + slot_of(ksq) * TILE_BYTES);
-      const uint32_t qb = smem_u32(sQ + h * TILE_BYTES);
+      const uint64_t kd = make_sdesc_sw128(smem_u32(sKV + slot_of(ksq) * TILE_BYTES), 16, 1024);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {  // head_dim 128 = 8 x K16; two 64-wide swizzle atoms
-        const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
-        umma_bf16_ss(tS[h], make_sdesc_sw128(qb + off, 16, 1024),
-                     make_sdesc_sw128(kb + off, 16, 1024), idesc_qk, kk > 0);
+        const uint64_t off = (uint64_t)(((kk >> 2) * ATOM_BYTES + (kk & 3) * 32) >> 4);
+        umma_bf16_ss(tS[h], qdesc[h] + off, kd + off, idesc_qk, kk > 0);
       }
     };
     auto issue_pv = [&](int h, uint32_t vsq, bool acc) {
-      const uint32_t vb = smem_u32(sKV + slot_of(vsq) * TILE_BYTES);
+      const uint64_t vd =
+          make_sdesc_sw128(smem_u32(sKV + slot_of(vsq) * TILE_BYTES), ATOM_BYTES, 1024);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {  // 128 kv rows = 8 x K16; P: 8 TMEM columns per step
-        umma_bf16_ts(tO[h], tS[h] + kk * 8, make_sdesc_sw128(vb + kk * 2048, ATOM_BYTES, 1024),
-                     idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        umma_bf16_ts(tO[h], tS[h] + kk * 8, vd + (uint64_t)((kk * 2048) >> 4), idesc_pv,
+                     (acc || kk > 0) ? 1u : 0u);
       }
     };
     int ws = 0, it = 0;
@@ -406,9 +413,23 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           for (int i = 0; i < 128; ++i)
             if (kv0 + i > qpos) sr[i] = -INFINITY;
         }
+#ifdef FP_ATTN_TREE_MAX
+        // 8 independent 3-input max chains, then a 3-level tree (latency ~ 16 dependent ops)
+        float mc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mc[k] = fmaxf(sr[k], sr[8 + k]);
+#pragma unroll
+        for (int i = 16; i < 128; i += 16) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mc[k] = fmaxf(mc[k], fmaxf(sr[i + k], sr[i + 8 + k]));
+        }
+        const float mx = fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])),
+                               fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7])));
+#else
         float mx = sr[0];
 #pragma unroll
         for (int i = 1; i < 128; ++i) mx = fmaxf(mx, sr[i]);
+#endif
         const float m_new = fmaxf(m, mx * sc);  // scaled (log2) units
         if (row == 0) ATTN_STAMP(it, j, 11 + 4 * h);
         if (j == 0) {

@@ -110,12 +110,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--len", type=int, action="append", default=[])
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--ours-only", action="store_true")
     a = ap.parse_args()
     from torch.nn.attention import SDPBackend
 
     for n in a.len or [4465]:
         flops = 4 * 4096 * n * (n + 1) / 2
         rows = [("ours (tcgen05, paged KV)", ours(n, a.reps))]
+        if a.ours_only:
+            print(f"n={n:6d} ours {rows[0][1] * 1e3:9.1f} us  {flops / rows[0][1] / 1e9:8.1f} TFLOP/s")
+            continue
         for name, be in (("torch sdpa cudnn", SDPBackend.CUDNN_ATTENTION),
                          ("torch sdpa flash", SDPBackend.FLASH_ATTENTION),
                          ("torch sdpa efficient", SDPBackend.EFFICIENT_ATTENTION)):

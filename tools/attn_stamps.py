@@ -34,7 +34,7 @@ def main():
     ap.add_argument("--len", type=int, default=4465)
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
-    os.environ["FP_AB_LIB"] = build_stamps()
+    os.environ["FP_AB_LIB"] = os.environ.get("FP_STAMPS_LIB") or build_stamps()
     os.environ["FP_GEMM_STAMPS"] = "1"
     import torch
 
