@@ -23,9 +23,13 @@
 //                exp2 online softmax with lazy O rescale (only when the row max grows by > 2^8),
 //                P written back to TMEM over S as bf16, final O / l epilogue to HBM.
 // Softmax arithmetic is budgeted against the tensor pipe: the scale is folded into one packed
-// FFMA2 per element pair, row sums use packed FADD2, and 3 of every 8 exponentials run as a
-// degree-3 polynomial on the FMA pipe (Cody-Waite split, |rel err| < 1.1e-4 -- below the bf16
-// rounding P gets anyway) so the 16/clk/SM MUFU.EX2 rate does not bound the loop.
+// FFMA2 per element pair, the row max is a tree of 8 chains, row sums use packed FADD2 after P
+// is released, and 2 of every 8 exponential pairs run as a degree-3 polynomial on the FMA pipe
+// (Cody-Waite split, |rel err| < 1.1e-4 -- below the bf16 rounding P gets anyway): MUFU.EX2
+// issues one warp instruction per ~8 cycles per SMSP, the exp phase's floor
+// (tools/attn_variants.sh: emulating 0 / 2 / 3 / 4 / 5 of 8 pairs).
+// The MMA warp builds descriptors once per 8-MMA group (tools/probes/mma_rate.cu: a descriptor
+// built per MMA cost more issue time than an N = 128 MMA executes).
 // TMEM columns: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
 #pragma once
 #include "common.cuh"
@@ -75,10 +79,7 @@ struct AttnTcParams {
 #endif
 
 namespace tcattn {
-constexpr int THREADS = 640;  // warpgroup 0: TMA + MMA warps (2 idle); warpgroups 1-4: softmax
-constexpr int REGS_CTRL = 32;    // setmaxnreg: warpgroup 0 gives registers to the softmax warps
-constexpr int REGS_SOFTMAX = 112;
-constexpr int REGS_COMMON = 96;  // launch allocation (640 threads): the shared tail runs at it
+constexpr int THREADS = 320;
 constexpr int TILE = 128;
 constexpr int TILE_BYTES = 128 * 128 * 2;  // 32 KB: two 64-column swizzle atoms of 16 KB
 constexpr int ATOM_BYTES = 16384;
@@ -91,7 +92,7 @@ constexpr int ATOM_BYTES = 16384;
 constexpr int STAGES = FP_ATTN_STAGES;
 constexpr int SMEM_BYTES = 1024 + 2 * TILE_BYTES + STAGES * TILE_BYTES + 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: rescale O only if max grows > 256x
-constexpr int SOFTMAX_WARPS = 16;
+constexpr int SOFTMAX_WARPS = 8;
 }  // namespace tcattn
 
 // ---- packed fp32 pairs (sm_100 FFMA2 / FADD2) -----------------------------------------------
@@ -202,8 +203,8 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     }
     for (int h = 0; h < 2; ++h) {
       mbar_init(&s_full[h], 1);
-      mbar_init(&p_full[h], 32 * SOFTMAX_WARPS / 2);
-      mbar_init(&o_empty[h], 32 * SOFTMAX_WARPS / 2);
+      mbar_init(&p_full[h], 128);
+      mbar_init(&o_empty[h], 128);
       mbar_init(&w_full[h], 1);
       mbar_init(&w_empty[h], 1 + SOFTMAX_WARPS);
     }
@@ -218,15 +219,10 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   grid_dep_wait();
   const bool run = guard_block(p.guard);
   const int n_work = p.n_items * p.n_kv_heads * p.pairs_per_kv;
-  // Warpgroup 0 (scheduler / TMA, MMA, 2 idle warps) hands registers to the softmax warpgroups.
-  // setmaxnreg is warpgroup-collective and ptxas gives each code region one register count, so
-  // it sits at the top of each warpgroup role's branch, and every role returns to the launch
-  // allocation before the common tail.
+
   if (!run) {
     // stopped at this boundary: nothing to do
-  } else if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_CTRL));
-    if (warp == 0) {
+  } else if (warp == 0) {
     // ------------------------------------------------------------ scheduler + TMA producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_last();  // K/V tiles are re-read by other q tiles
@@ -279,7 +275,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       }
     }
     __syncwarp();
-    } else if (warp == 1) {
+  } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, false);
     constexpr uint32_t idesc_pv = make_idesc_bf16(128, 128, true);  // V is MN-major
@@ -382,28 +378,15 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       tc += n_tiles;
       ++it;
     }
-    }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_COMMON));
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_SOFTMAX));
     // ------------------------------------------------------------------ softmax + epilogue
-    // 16 warps (warpgroups 1-4), 8 per head, TWO per TMEM lane quadrant (a warp reaches only the lanes of quadrant
-    // warp % 4): warp (quadrant q, half u) owns lanes [32q + 16u, +16) through the 16-lane TMEM
-    // shapes. Thread t holds rows rl = 32q + 16u + t/4 and rl + 8, columns {8k + 2(t%4), +1}:
-    // a row is spread over the 4 threads t%4 = 0..3 (max by two xor-shuffles), and two warps
-    // per SMSP per head give the exponential stream the latency hiding one warp lacks
-    // (tools/attn_stamps.py: the exp phase ran at ~half the SMSP issue rate with one).
-    const int h = (warp - 4) >> 3;         // 0: warps 4-11, 1: warps 12-19
-    const int quad = warp & 3;
-    const int half = ((warp - 4) >> 2) & 1;
-    const int lbase = quad * 32 + half * 16;
-    const int j4 = lane & 3;
-    const int rl = lbase + (lane >> 2);    // rows rl, rl + 8 of the 128-row query tile
-    const uint32_t lane_off = (uint32_t)lbase << 16;
+    const int h = (warp - 2) >> 2;  // 0: warps 2-5, 1: warps 6-9
+    const int quad = warp & 3;      // TMEM lane quadrant accessible to this warp
+    const int row = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t tS = tbase + h * 128 + lane_off;
     const uint32_t tO = tbase + 256 + h * 128 + lane_off;
     const float sc = p.scale_log2;
-    const uint32_t FULL = 0xffffffffu;
     int ws = 0, it = 0;
     uint32_t wph = 0, tc = 0;
     for (;;) {
@@ -417,149 +400,128 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       }
       if (w < 0) break;
       const AttnWork a = attn_decode(p, w);
-      const int qp0 = a.it.q_pos0 + rl;  // positions of rows rl and rl + 8
-      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+      const int qpos = a.it.q_pos0 + row;
+      float m = -INFINITY, l = 0.f;
       for (int j = 0; j < a.n_tiles; ++j) {
         mbar_wait(&s_full[h], (tc + j) & 1);
         tc_fence_after();
-        if (rl == 0) ATTN_STAMP(it, j, 2 * h);
-        uint32_t su[64];  // register 4k + 2r + b: row rl + 8r, column 8k + 2 j4 + b
-        tmem_ld16x256_x16(tS, su);
+        if (row == 0) ATTN_STAMP(it, j, 2 * h);
+        uint32_t su[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, su[c]);
         tmem_ld_wait();
-        if (rl == 0) ATTN_STAMP(it, j, 10 + 4 * h);
+        float sr[128];
+#pragma unroll
+        for (int i = 0; i < 128; ++i) sr[i] = __uint_as_float(su[i >> 5][i & 31]);
+        if (row == 0) ATTN_STAMP(it, j, 10 + 4 * h);
         const int kv0 = j * TILE;
         if (kv0 + TILE - 1 > a.it.q_pos0) {  // diagonal tile: causal mask
 #pragma unroll
-          for (int k = 0; k < 16; ++k)
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int b = 0; b < 2; ++b)
-                if (kv0 + 8 * k + 2 * j4 + b > qp0 + 8 * r)
-                  su[4 * k + 2 * r + b] = __float_as_uint(-INFINITY);
+          for (int i = 0; i < 128; ++i)
+            if (kv0 + i > qpos) sr[i] = -INFINITY;
         }
-        float mx0, mx1;
-        {
-          float c0[4], c1[4];  // 4 independent chains per row
+#ifndef FP_ATTN_CHAIN_MAX
+        // 8 independent 3-input max chains, then a 3-level tree (latency ~ 16 dependent ops)
+        float mc[8];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            c0[q] = fmaxf(__uint_as_float(su[4 * q]), __uint_as_float(su[4 * q + 1]));
-            c1[q] = fmaxf(__uint_as_float(su[4 * q + 2]), __uint_as_float(su[4 * q + 3]));
-          }
+        for (int k = 0; k < 8; ++k) mc[k] = fmaxf(sr[k], sr[8 + k]);
 #pragma unroll
-          for (int k = 4; k < 16; ++k) {
-            c0[k & 3] = fmaxf(c0[k & 3], fmaxf(__uint_as_float(su[4 * k]), __uint_as_float(su[4 * k + 1])));
-            c1[k & 3] = fmaxf(c1[k & 3], fmaxf(__uint_as_float(su[4 * k + 2]), __uint_as_float(su[4 * k + 3])));
-          }
-          mx0 = fmaxf(fmaxf(c0[0], c0[1]), fmaxf(c0[2], c0[3]));
-          mx1 = fmaxf(fmaxf(c1[0], c1[1]), fmaxf(c1[2], c1[3]));
+        for (int i = 16; i < 128; i += 16) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mc[k] = fmaxf(mc[k], fmaxf(sr[i + k], sr[i + 8 + k]));
         }
-        mx0 = fmaxf(mx0, __shfl_xor_sync(FULL, mx0, 1));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(FULL, mx1, 1));
-        mx0 = fmaxf(mx0, __shfl_xor_sync(FULL, mx0, 2));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(FULL, mx1, 2));
-        const float mn0 = fmaxf(m0, mx0 * sc), mn1 = fmaxf(m1, mx1 * sc);  // log2 units
-        if (rl == 0) ATTN_STAMP(it, j, 11 + 4 * h);
+        const float mx = fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])),
+                               fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7])));
+#else
+        float mx = sr[0];
+#pragma unroll
+        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, sr[i]);
+#endif
+        const float m_new = fmaxf(m, mx * sc);  // scaled (log2) units
+        if (row == 0) ATTN_STAMP(it, j, 11 + 4 * h);
         if (j == 0) {
-          m0 = mn0;
-          m1 = mn1;
+          m = m_new;
         } else {
-          const bool need0 = mn0 > m0 + RESCALE_THRESHOLD, need1 = mn1 > m1 + RESCALE_THRESHOLD;
-          if (__any_sync(FULL, need0 || need1)) {
-            const float al0 = need0 ? fast_exp2(m0 - mn0) : 1.f;
-            const float al1 = need1 ? fast_exp2(m1 - mn1) : 1.f;
-            if (need0) {
-              l0 *= al0;
-              m0 = mn0;
-            }
-            if (need1) {
-              l1 *= al1;
-              m1 = mn1;
+          const bool need = m_new > m + RESCALE_THRESHOLD;
+          if (__any_sync(0xffffffffu, need)) {
+            const float alpha = need ? fast_exp2(m - m_new) : 1.f;
+            if (need) {
+              l *= alpha;
+              m = m_new;
             }
 #pragma unroll 1
-            for (int c = 0; c < 2; ++c) {  // O rows, two 64-column halves
+            for (int c = 0; c < 4; ++c) {
               uint32_t o[32];
-              tmem_ld16x256_x8(tO + c * 64, o);
+              tmem_ld32(tO + c * 32, o);
               tmem_ld_wait();
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                o[4 * k] = __float_as_uint(__uint_as_float(o[4 * k]) * al0);
-                o[4 * k + 1] = __float_as_uint(__uint_as_float(o[4 * k + 1]) * al0);
-                o[4 * k + 2] = __float_as_uint(__uint_as_float(o[4 * k + 2]) * al1);
-                o[4 * k + 3] = __float_as_uint(__uint_as_float(o[4 * k + 3]) * al1);
-              }
-              tmem_st16x256_x8(tO + c * 64, o);
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(tO + c * 32, o);
             }
             tmem_st_wait();
           }
         }
-        const float nm0 = (m0 == -INFINITY) ? 0.f : -m0;
-        const float nm1 = (m1 == -INFINITY) ? 0.f : -m1;
-        // P: the pair (row rl + 8r, columns 8k + 2 j4, +1) is P word 4k + j4 of that row, i.e.
-        // register 2k + r of the 16x128b store
-        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+        const float nm = (m == -INFINITY) ? 0.f : -m;
 #pragma unroll
-        for (int hk = 0; hk < 2; ++hk) {  // two halves of 32 P columns: 16 live pack registers
+        for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const int k = hk * 8 + kk;
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const float nm = r ? nm1 : nm0;
-              const float2 x = ffma2(make_float2(__uint_as_float(su[4 * k + 2 * r]),
-                                                 __uint_as_float(su[4 * k + 2 * r + 1])),
-                                     make_float2(sc, sc), make_float2(nm, nm));
-              float2 e;
-              if (kk < FP_ATTN_EMU) {  // EMU of every 8 pairs on the FMA pipe
-                e = exp2_poly2(x);
-              } else {
-                e.x = fast_exp2(x.x);
-                e.y = fast_exp2(x.y);
-              }
-              if (r) s1 = fadd2(s1, e);
-              else s0 = fadd2(s0, e);
-              pk[2 * kk + r] = pack_bf16x2(e.x, e.y);
+          for (int i = 0; i < 32; i += 2) {
+            const float2 x = ffma2(make_float2(sr[c * 32 + i], sr[c * 32 + i + 1]),
+                                   make_float2(sc, sc), make_float2(nm, nm));
+            float2 e;
+            if (((i & 15) >> 1) < FP_ATTN_EMU) {  // EMU of every 8 pairs on the FMA pipe
+              e = exp2_poly2(x);
+            } else {
+              e.x = fast_exp2(x.x);
+              e.y = fast_exp2(x.y);
             }
+            sr[c * 32 + i] = e.x;  // kept for the row sum, taken after P is released
+            sr[c * 32 + i + 1] = e.y;
+            pk[i >> 1] = pack_bf16x2(e.x, e.y);
           }
-          tmem_st16x128_x8(tS + hk * 32, pk);  // P (bf16 pairs) over the first 64 columns of S
+          tmem_st16(tS + c * 16, pk);  // P (bf16 pairs) over the consumed S columns
         }
-        if (rl == 0) ATTN_STAMP(it, j, 12 + 4 * h);
+        if (row == 0) ATTN_STAMP(it, j, 12 + 4 * h);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[h]);
-        if (rl == 0) ATTN_STAMP(it, j, 2 * h + 1);
-        l0 += s0.x + s0.y;
-        l1 += s1.x + s1.y;
-        if (rl == 0) ATTN_STAMP(it, j, 13 + 4 * h);
+        if (row == 0) ATTN_STAMP(it, j, 2 * h + 1);
+        // row sum off the P -> PV critical path (same pairing and order as before)
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 128; i += 2) {
+          const float2 e = make_float2(sr[i], sr[i + 1]);
+          if (i & 2) acc1 = fadd2(acc1, e);
+          else acc0 = fadd2(acc0, e);
+        }
+        l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+        if (row == 0) ATTN_STAMP(it, j, 13 + 4 * h);
       }
-      // epilogue: O / l -> bf16 -> HBM (row sums: the 4 threads of a row), then release O
-      l0 += __shfl_xor_sync(FULL, l0, 1);
-      l1 += __shfl_xor_sync(FULL, l1, 1);
-      l0 += __shfl_xor_sync(FULL, l0, 2);
-      l1 += __shfl_xor_sync(FULL, l1, 2);
+      // epilogue: O / l -> bf16 -> HBM, then release O for the next item's first P*V
       mbar_wait(o_full, it & 1);
       tc_fence_after();
-      const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
-      const bool head_live = h == 0 || a.has_head1;
-      const int head = h ? a.head1 : a.head0;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const bool live = row < a.it.n_rows && (h == 0 || a.has_head1);
+      __nv_bfloat16* dst =
+          p.out + (long long)(a.it.q_row0 + row) * p.ldo + (h ? a.head1 : a.head0) * 128;
 #pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t o[32];
-        tmem_ld16x256_x8(tO + c * 64, o);
+        tmem_ld32(tO + c * 32, o);
         tmem_ld_wait();
+        if (live) {
+          float v[32];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int row = rl + 8 * r;
-          if (head_live && row < a.it.n_rows) {
-            const float inv = r ? inv1 : inv0;
-            __nv_bfloat16* dst = p.out + (long long)(a.it.q_row0 + row) * p.ldo + head * 128 +
-                                 c * 64 + 2 * j4;
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * inv;
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              *reinterpret_cast<uint32_t*>(dst + 8 * k) =
-                  pack_bf16x2(__uint_as_float(o[4 * k + 2 * r]) * inv,
-                              __uint_as_float(o[4 * k + 2 * r + 1]) * inv);
+          for (int i = 0; i < 4; ++i) {
+            uint4 u;
+            u.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+            u.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+            u.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+            u.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+            st_global_v4(dst + c * 32 + 8 * i, u);
           }
         }
       }
@@ -568,7 +530,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       tc += a.n_tiles;
       ++it;
     }
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_COMMON));
   }
   tc_fence_before();
   __syncthreads();
