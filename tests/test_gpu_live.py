@@ -14,7 +14,7 @@ def test_live_config1_trace(golden_dir):
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.config import SHAPES
     from paper_2602_16603_b200.engine import synthetic_tokens
-    from paper_2602_16603_b200.live import run_live
+    from paper_2602_16603_b200.live import replay_rounds, run_live
     from paper_2602_16603_b200.native import PrefillContext
 
     ps = refsim_or_skip()
@@ -25,11 +25,16 @@ def test_live_config1_trace(golden_dir):
     ctx.load_weights(F.make_weights(shape, 1234))
     # cost model only weights progress() and the predictor; scaled to the tiny model on B200
     params = ps.CostParams(num_layers=4)
+    rounds: list = []
     res = run_live(trace, ps.PolicyConfig(), params, ctx, synthetic_tokens(1234, shape.vocab),
-                   record_events=True, max_wall_s=120)
+                   record_events=True, max_wall_s=120, round_log=rounds)
     assert sorted(o.id for o in res.outcomes) == sorted(r.id for r in trace.requests)
     assert res.rounds == len(trace) + len(res.tasks)
-    assert res.commands["resume"] == res.commands["preempt"]
+    # every preempted task resumes, except one whose ACK lost the race with its own completion
+    # (completion wins: engine.py:279-291)
+    raced = sum(1 for r in rounds if r.get("completed"))
+    assert res.commands["resume"] == res.commands["preempt"] - raced
+    replay_rounds(trace, ps.PolicyConfig(), params, rounds)
     assert len(res.blocking_log) == res.commands["preempt"]
     for sig, ack, _ in res.blocking_log:
         assert ack - sig < 0.05
@@ -46,7 +51,7 @@ def test_live_preemption_llama_shape():
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.config import SHAPES
     from paper_2602_16603_b200.engine import synthetic_tokens
-    from paper_2602_16603_b200.live import run_live
+    from paper_2602_16603_b200.live import replay_rounds, run_live
     from paper_2602_16603_b200.native import PrefillContext
 
     ps = refsim_or_skip()
@@ -63,11 +68,14 @@ def test_live_preemption_llama_shape():
         reqs.append(ps.Request(i, "text", 0.006 * i, 300 + 50 * i, 0.3))
     trace = ps.Trace(tuple(reqs))
     params = ps.CostParams(num_layers=4)
+    rounds: list = []
     res = run_live(trace, ps.PolicyConfig(), params, ctx, synthetic_tokens(0, shape.vocab),
-                   record_events=True, max_wall_s=120)
+                   record_events=True, max_wall_s=120, round_log=rounds)
     assert sorted(o.id for o in res.outcomes) == list(range(6))
     assert res.commands["preempt"] >= 1
-    assert res.commands["resume"] == res.commands["preempt"]
+    raced = sum(1 for r in rounds if r.get("completed"))  # completion won the ACK race
+    assert res.commands["resume"] == res.commands["preempt"] - raced
+    replay_rounds(trace, ps.PolicyConfig(), params, rounds)
     bl = ps.blocking_stats(res.blocking_log)
     print("live llama4L:", res.commands, ps.slo_attainment(res.outcomes), bl)
     assert bl["max_s"] < 0.02  # one operator at 16K tokens is a few ms on a B200
