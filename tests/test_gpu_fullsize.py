@@ -184,3 +184,36 @@ def test_llama_layer_dims_vs_oracle():
             print(f"len {lens[i]}: alone vs batched {rel(la, lb[i]):.4f}")
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("chunk,lens", [(512, [1300, 200]), (2048, [2200, 100])])
+def test_llama_layer_dims_chunked_vs_oracle(chunk, lens):
+    """Chunked prefill at the Llama-3-8B layer dimensions (2 layers, vocab 8192) against the
+    oracle running the same chunk plan (cost_model.py:214-233): a long and a short request
+    batched, chunks of 512 / 2048 (3 / 2 chunks, the short request's share split across a chunk
+    boundary) -- logits and the last layer's KV within the stated bf16 tolerance."""
+    from dataclasses import replace
+
+    from oracle import forward as F
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    oshape = F.Shape(2, 4096, 32, 8, 128, 14336, 8192, 5e5)
+    w = F.make_weights(oshape, 8)
+    gshape = replace(SHAPES["llama3-8b"], num_layers=2, vocab=8192)
+    c = PrefillContext(gshape, kv_pages=64, page_size=128, max_pos=8192)
+    try:
+        c.load_weights(w)
+        tokens = F.make_tokens(lens, oshape.vocab, 5)
+        ot = F.OracleTask(oshape, w, tokens, chunk)
+        ot.run_all()
+        t = run(c, tokens, chunk)
+        assert t.n_entries == 5 * 2 * -(-sum(lens) // chunk)
+        P.logits(f"llama3-8b dims 2L chunk {chunk}", t.logits(), ot.logits)
+        for i in range(2):
+            k, v = t.read_kv(i, 1)
+            P.kv(f"llama3-8b dims 2L chunk {chunk} K[{i}][1]", k, ot.k_cache[i][1])
+            P.kv(f"llama3-8b dims 2L chunk {chunk} V[{i}][1]", v, ot.v_cache[i][1])
+        t.destroy()
+    finally:
+        c.close()
