@@ -72,9 +72,20 @@ struct AttnTcParams {
     if (p.dbg && (it) == 0 && blockIdx.x < 16 && (j) < 64)                                 \
       p.dbg[((int)blockIdx.x * 64 + (j)) * 24 + (k)] = (unsigned long long)clock64();       \
   } while (0)
+// Per work item (items 0..31 of CTAs 0..15) at [24576 + (cta * 32 + item) * 8 + k]: MMA warp
+// got the item (0), issued its first Q*K^T (1); head-0 softmax row 0: first S seen (2), last P
+// out (3), O complete seen (4), epilogue done (5); kernel-relative start of the CTA (6, item 0).
+#define ATTN_ISTAMP(it, k)                                                                \
+  do {                                                                                    \
+    if (p.dbg && (it) < 32 && blockIdx.x < 16)                                             \
+      p.dbg[24576 + ((int)blockIdx.x * 32 + (it)) * 8 + (k)] = (unsigned long long)clock64(); \
+  } while (0)
 #else
 #define ATTN_STAMP(it, j, k) \
   do {                       \
+  } while (0)
+#define ATTN_ISTAMP(it, k) \
+  do {                     \
   } while (0)
 #endif
 
@@ -217,6 +228,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   grid_dep_wait();
+  if (threadIdx.x == 0) ATTN_ISTAMP(0, 6);
   const bool run = guard_block(p.guard);
   const int n_work = p.n_items * p.n_kv_heads * p.pairs_per_kv;
 
@@ -319,9 +331,11 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       }
       if (w < 0) break;
       const int n_tiles = attn_decode(p, w).n_tiles;
+      if (lane == 0) ATTN_ISTAMP(it, 0);
       mbar_wait(q_full, it & 1);
       wait_tile(seq);
       tc_fence_after();
+      if (lane == 0) ATTN_ISTAMP(it, 1);
       if (lane == 0) {
         issue_qk(0, seq);
         tc_commit(&s_full[0]);
@@ -406,6 +420,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         mbar_wait(&s_full[h], (tc + j) & 1);
         tc_fence_after();
         if (row == 0) ATTN_STAMP(it, j, 2 * h);
+        if (row == 0 && h == 0 && j == 0) ATTN_ISTAMP(it, 2);
         uint32_t su[4][32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, su[c]);
@@ -487,6 +502,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         tc_fence_before();
         mbar_arrive(&p_full[h]);
         if (row == 0) ATTN_STAMP(it, j, 2 * h + 1);
+        if (row == 0 && h == 0 && j == a.n_tiles - 1) ATTN_ISTAMP(it, 3);
         // row sum off the P -> PV critical path (same pairing and order as before)
         float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -501,6 +517,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       // epilogue: O / l -> bf16 -> HBM, then release O for the next item's first P*V
       mbar_wait(o_full, it & 1);
       tc_fence_after();
+      if (row == 0 && h == 0) ATTN_ISTAMP(it, 4);
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const bool live = row < a.it.n_rows && (h == 0 || a.has_head1);
       __nv_bfloat16* dst =
@@ -527,6 +544,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&o_empty[h]);
+      if (row == 0 && h == 0) ATTN_ISTAMP(it, 5);
       tc += a.n_tiles;
       ++it;
     }

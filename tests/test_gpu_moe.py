@@ -114,8 +114,11 @@ def check_routing(t, ot, w_router, k, exact):
     assert same[decisive].all(), np.nonzero(decisive & ~same)
     assert same.mean() >= 0.96, same.mean()
     o_gpu, o_ref = np.argsort(ids, -1), np.argsort(ot.moe_ids, -1)
+    # router weights are probabilities: layer 0 sees only the embedding (one bf16 GEMM away
+    # from fp32), the last layer the whole bf16 stack below it
+    atol = 5e-2 if exact else 8e-2
     np.testing.assert_allclose(np.take_along_axis(wts, o_gpu, -1)[same],
-                               np.take_along_axis(ot.moe_w, o_ref, -1)[same], rtol=0, atol=5e-2)
+                               np.take_along_axis(ot.moe_w, o_ref, -1)[same], rtol=0, atol=atol)
 
 
 def test_moe_deterministic_and_batch_independent(moe):

@@ -97,6 +97,33 @@ def main():
         print(f"  median softmax latency h0 {np.median(sm0):.0f} h1 {np.median(sm1):.0f} cycles; "
               f"P->next S h0 {np.median(s2s0):.0f}; period per tile {np.median(per):.0f}; "
               f"ideal TC per tile (2 heads, 8192 flop/clk) {2 * 4 * 128 ** 3 / 8192:.0f}")
+    # per work item: where the time between items goes
+    it = buf.reshape(-1)[24576: 24576 + 16 * 32 * 8].reshape(16, 32, 8).astype(np.int64)
+    gaps = {"item fetch -> first QK issued": [], "first QK -> first S seen": [],
+            "last P -> O complete": [], "epilogue": [], "epilogue done -> next item's first S": []}
+    spans = []
+    for cta in range(16):
+        t = it[cta]
+        n = int((t[:, 2] > 0).sum())
+        for i in range(n):
+            if t[i, 1] and t[i, 0]:
+                gaps["item fetch -> first QK issued"].append(t[i, 1] - t[i, 0])
+            if t[i, 2] and t[i, 1]:
+                gaps["first QK -> first S seen"].append(t[i, 2] - t[i, 1])
+            if t[i, 4] and t[i, 3]:
+                gaps["last P -> O complete"].append(t[i, 4] - t[i, 3])
+            if t[i, 5] and t[i, 4]:
+                gaps["epilogue"].append(t[i, 5] - t[i, 4])
+            if i + 1 < n and t[i + 1, 2] and t[i, 5]:
+                gaps["epilogue done -> next item's first S"].append(t[i + 1, 2] - t[i, 5])
+        if n and t[0, 6]:
+            spans.append((t[n - 1, 5] - t[0, 6], t[0, 2] - t[0, 6], n))
+    for k, v in gaps.items():
+        if v:
+            print(f"  per item: {k:40s} median {np.median(v):7.0f} cycles (n={len(v)})")
+    if spans:
+        print(f"  CTA span (cycles): median {np.median([s[0] for s in spans]):.0f}; kernel start -> "
+              f"first S {np.median([s[1] for s in spans]):.0f}; items per CTA {np.median([s[2] for s in spans]):.0f}")
     c.close()
 
 
