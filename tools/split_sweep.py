@@ -34,7 +34,7 @@ def main():
         for M in MS:
             A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
             C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-            for pair, S in [(-1, 0), (2, 0)] + [(pair, S) for pair in (0, 1) for S in SPLITS]:
+            for pair, S in [(-1, 0), (2, 0), (3, 0)] + [(pair, S) for pair in (0, 1) for S in SPLITS]:
                 if True:
                     lib.fp_ctx_set_gemm_policy(ctx.h, pair, S)
                     i = [0]
@@ -60,9 +60,10 @@ def main():
             lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
             best = min((r for r in res if r["N"] == N and r["K"] == K and r["M"] == M),
                        key=lambda r: r["us"])
-            print(f"N={N} K={K} M={M}: best pair={best['pair']} S={best['S']} "
-                  f"{best['us']} us",
-                  flush=True)
+            auto = next(r for r in res if r["N"] == N and r["K"] == K and r["M"] == M
+                        and r["pair"] == -1)
+            print(f"N={N} K={K} M={M}: auto {auto['us']} us, best pair={best['pair']} "
+                  f"S={best['S']} {best['us']} us ({auto['us'] / best['us']:.2f}x)", flush=True)
         del Bs
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as fh:
