@@ -248,7 +248,8 @@ int fp_op_tp_allreduce(fp_ctx** ctxs, int32_t n, void* const* h, const void* con
                        int32_t M);
 
 /* ---- per-operator entry points (device pointers; unit tests and microbenchmarks) -------- */
-/* C[M,N] = A[M,K] B[N,K]^T; epi: 0 bf16 store, 1 fp32 store, 2 residual add into C (bf16). */
+/* C[M,N] = A[M,K] B[N,K]^T; epi: 0 bf16 store, 1 fp32 store, 2 residual add into C (bf16),
+ * 3 SwiGLU: B packed [gate(128) | up(128)] per 256 rows, C[M, N/2] = silu(gate) * up. */
 int fp_op_gemm(fp_ctx* ctx, int32_t epi, const void* A, const void* B, void* C, int32_t M,
                int32_t N, int32_t K);
 int fp_op_rmsnorm(fp_ctx* ctx, const void* x, const void* gamma, void* out, int32_t M,

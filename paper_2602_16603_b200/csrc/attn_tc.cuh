@@ -101,7 +101,9 @@ constexpr int ATOM_BYTES = 16384;
 #define FP_ATTN_STAGES 3
 #endif
 constexpr int STAGES = FP_ATTN_STAGES;
-constexpr int SMEM_BYTES = 1024 + 2 * TILE_BYTES + STAGES * TILE_BYTES + 512;
+// Q tiles (2 heads), the K/V ring, barriers, and one 32 KB output staging tile per head (the
+// epilogue writes O there in the 128B-swizzled layout and TMA stores it: coalesced)
+constexpr int SMEM_BYTES = 1024 + 2 * TILE_BYTES + STAGES * TILE_BYTES + 512 + 2 * TILE_BYTES;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: rescale O only if max grows > 256x
 constexpr int SOFTMAX_WARPS = 8;
 }  // namespace tcattn
@@ -179,7 +181,8 @@ DEVI AttnWork attn_decode(const AttnTcParams& p, int w) {
 
 __global__ void __launch_bounds__(tcattn::THREADS, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
-                           const __grid_constant__ CUtensorMap tmKV, const AttnTcParams p) {
+                           const __grid_constant__ CUtensorMap tmKV,
+                           const __grid_constant__ CUtensorMap tmO, const AttnTcParams p) {
   using namespace tcattn;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -193,12 +196,13 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   uint64_t* kv_empty = kv_full + STAGES;
   uint64_t* s_full = kv_empty + STAGES;  // [2]
   uint64_t* p_full = s_full + 2;         // [2]
-  uint64_t* o_full = p_full + 2;
-  uint64_t* o_empty = o_full + 1;        // [2]
+  uint64_t* o_full = p_full + 2;         // [2] per head: the item's last P*V done
+  uint64_t* o_empty = o_full + 2;        // [2]
   uint64_t* w_full = o_empty + 2;        // [2] work ring
   uint64_t* w_empty = w_full + 2;        // [2]
   int* w_ring = reinterpret_cast<int*>(w_empty + 2);  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_ring + 2);
+  uint8_t* sOut = sKV + STAGES * TILE_BYTES + 512;  // [2 heads][TILE_BYTES] output staging
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -216,10 +220,10 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       mbar_init(&s_full[h], 1);
       mbar_init(&p_full[h], 128);
       mbar_init(&o_empty[h], 128);
+      mbar_init(&o_full[h], 1);
       mbar_init(&w_full[h], 1);
       mbar_init(&w_empty[h], 1 + SOFTMAX_WARPS);
     }
-    mbar_init(o_full, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -356,7 +360,10 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         if (j == 0) mbar_wait(&o_empty[0], (it & 1) ^ 1);  // previous item's O0 drained
         tc_fence_after();
         if (lane == 0) ATTN_STAMP(it, j, 4);
-        if (lane == 0) issue_pv(0, vsq, j > 0);
+        if (lane == 0) {
+          issue_pv(0, vsq, j > 0);
+          if (last) tc_commit(&o_full[0]);  // head 0's epilogue need not wait for head 1
+        }
         __syncwarp();
         if (!last) {
           wait_tile(ksq);
@@ -375,6 +382,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         if (lane == 0) ATTN_STAMP(it, j, 6);
         if (lane == 0) {
           issue_pv(1, vsq, j > 0);
+          if (last) tc_commit(&o_full[1]);
           tc_commit(&kv_empty[slot_of(vsq)]);
           if (!last) {
             issue_qk(1, ksq);
@@ -387,8 +395,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         __syncwarp();
         seq += last ? 1 : 2;  // the last step consumes V only; the next item's K_0 follows
       }
-      if (lane == 0) tc_commit(o_full);
-      __syncwarp();
       tc += n_tiles;
       ++it;
     }
@@ -515,7 +521,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         if (row == 0) ATTN_STAMP(it, j, 13 + 4 * h);
       }
       // epilogue: O / l -> bf16 -> HBM, then release O for the next item's first P*V
-      mbar_wait(o_full, it & 1);
+      mbar_wait(&o_full[h], it & 1);
       tc_fence_after();
       if (row == 0 && h == 0) ATTN_ISTAMP(it, 4);
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -524,14 +530,45 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           p.out + (long long)(a.it.q_row0 + row) * p.ldo + (h ? a.head1 : a.head0) * 128;
       // all of O in registers with one wait (the S registers are dead here), then release O at
       // once -- the next item's first P*V may overwrite it while these rows are stored
-      // (tools/attn_stamps.py: the per-chunk load / wait / store epilogue took ~5400 cycles)
       uint32_t o[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tO + c * 32, o[c]);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&o_empty[h]);
-      if (live) {
+      if (a.it.n_rows == TILE) {
+        // full tile: rows -> the head's staging tile (two 64-column 128B-swizzled atoms, the
+        // layout TMA reads), then one thread stores it with two TMA boxes. Row-per-thread
+        // global stores were uncoalesced (16 B into 32 different lines per instruction): ~5200
+        // cycles per item (tools/attn_stamps.py).
+        uint8_t* stg = sOut + h * TILE_BYTES;
+        const uint32_t bar_id = 1 + h;  // named barrier of this head's 128 softmax threads
+        if (row == 0) bulk_wait_group_read0();  // the previous item's store has read the tile
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        if (h == 0 || a.has_head1) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {  // 16-byte chunk k of the row: atom k / 8, chunk k % 8
+            const int c = k >> 2, i = k & 3;
+            uint4 u;
+            u.x = pack_bf16x2(__uint_as_float(o[c][8 * i + 0]) * inv, __uint_as_float(o[c][8 * i + 1]) * inv);
+            u.y = pack_bf16x2(__uint_as_float(o[c][8 * i + 2]) * inv, __uint_as_float(o[c][8 * i + 3]) * inv);
+            u.z = pack_bf16x2(__uint_as_float(o[c][8 * i + 4]) * inv, __uint_as_float(o[c][8 * i + 5]) * inv);
+            u.w = pack_bf16x2(__uint_as_float(o[c][8 * i + 6]) * inv, __uint_as_float(o[c][8 * i + 7]) * inv);
+            *reinterpret_cast<uint4*>(stg + (k >> 3) * ATOM_BYTES + row * 128 +
+                                      (((k & 7) ^ (row & 7)) << 4)) = u;
+          }
+          fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA (async proxy)
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        if (row == 0 && (h == 0 || a.has_head1)) {
+          const int col = (h ? a.head1 : a.head0) * 128;
+          tma_store_2d(&tmO, stg, col, a.it.q_row0);
+          tma_store_2d(&tmO, stg + ATOM_BYTES, col + 64, a.it.q_row0);
+          bulk_commit_group();
+        }
+      } else if (live) {
+        // partial tile (a request's last rows): only the live rows -- the rows after them
+        // belong to the next request
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
 #pragma unroll
@@ -549,6 +586,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
       tc += a.n_tiles;
       ++it;
     }
+    if (row == 0) bulk_wait_group0();  // this head's TMA stores complete before the CTA exits
   }
   tc_fence_before();
   __syncthreads();

@@ -596,6 +596,7 @@ static int launch_rms(const RmsParams& p, cudaStream_t st) {
 }
 
 static void launch_attn(const fp_ctx* c, const CUtensorMap& tq, const CUtensorMap& tkv,
+                        const CUtensorMap& to,
                         const AttnTcParams& p, cudaStream_t st) {
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, c->device, [] {
@@ -605,7 +606,7 @@ static void launch_attn(const fp_ctx* c, const CUtensorMap& tq, const CUtensorMa
   // persistent: one CTA per SM (at most one per work item), work taken longest-first
   const int n_work = p.n_items * p.n_kv_heads * p.pairs_per_kv;
   launch_pdl(attn_prefill_tc_kernel, dim3(std::min(n_work, c->num_sms)), dim3(tcattn::THREADS),
-             tcattn::SMEM_BYTES, st, tq, tkv, p);
+             tcattn::SMEM_BYTES, st, tq, tkv, to, p);
 }
 
 static bool boundary_eligible(const fp_ctx* c, int gran, int i, int n_entries) {
@@ -866,7 +867,7 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
     a.guard = g;
     if (a.n_items > 0) {
       ProfScope ps(c, st, FP_K_ATTN, layer, M, ch.attn_flops, 0.0);
-      launch_attn(c, t->tm_q, c->tm_kv, a, st);
+      launch_attn(c, t->tm_q, c->tm_kv, t->tm_ao, a, st);  // out = ao (map: 128-row boxes)
     }
   } else {  // O_PROJ / DOWN_PROJ: residual add (tensor parallel: partial sum + all-reduce)
     GemmParams p{};
@@ -2066,7 +2067,10 @@ int fp_op_gemm(fp_ctx* c, int32_t epi, const void* A, const void* B, void* C, in
   if (epi == 0) launch_gemm<EPI_STORE_BF16>(c, ta, tb, p, c->stream);
   else if (epi == 1) launch_gemm<EPI_STORE_F32>(c, ta, tb, p, c->stream);
   else if (epi == 2) launch_gemm<EPI_RESID>(c, ta, tb, p, c->stream);
-  else return set_err(FP_ERR_ARG, "bad epilogue");
+  else if (epi == 3) {  // SwiGLU over B already packed [gate(128) | up(128)] per 256 rows
+    p.ldo = N / 2;
+    launch_gemm<EPI_SWIGLU>(c, ta, tb, p, c->stream);
+  } else return set_err(FP_ERR_ARG, "bad epilogue");
   CK(cudaGetLastError());
   return FP_OK;
 }
@@ -2187,8 +2191,9 @@ int fp_op_attn_prefill(fp_ctx* c, const void* q, const void* k, const void* v, v
                      st));
   CK(cudaMemcpyAsync(meta + items.size() * sizeof(AttnTile), pages.data(), pages.size() * 4,
                      cudaMemcpyHostToDevice, st));
-  CUtensorMap tq;
+  CUtensorMap tq, to;
   int rc = make_map(&tq, q, n_q, c->qdim, 128);
+  if (rc == FP_OK) rc = make_map(&to, out, n_q, c->qdim, 128);
   if (rc == FP_OK) {
     AttnTcParams a{};
     a.items = reinterpret_cast<const AttnTile*>(meta);
@@ -2205,7 +2210,7 @@ int fp_op_attn_prefill(fp_ctx* c, const void* q, const void* k, const void* v, v
     a.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
     a.sched = c->attn_sched;
     a.dbg = c->gemm_dbg;
-    launch_attn(c, tq, c->tm_kv, a, st);
+    launch_attn(c, tq, c->tm_kv, to, a, st);
   }
   CK(cudaFreeAsync(meta, st));
   CK(cudaStreamSynchronize(st));

@@ -15,6 +15,7 @@ from paper_2602_16603_b200.config import SHAPES  # noqa: E402
 from paper_2602_16603_b200.native import PrefillContext  # noqa: E402
 
 SHAPES_NK = [(4096, 4096), (6144, 4096), (28672, 4096), (4096, 14336)]
+EPI = {(28672, 4096): 3}  # gate_up: the SwiGLU epilogue (packed gate/up weights); others residual
 MS = [42, 163, 386, 545, 872, 1021, 1572, 2048, 3000]
 SPLITS = [1, 2, 3, 4, 6, 8, 12, 16]
 
@@ -23,12 +24,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/split_sweep.json")
     ap.add_argument("--iters", type=int, default=12)
+    ap.add_argument("--shapes", default="", help="N,K;N,K subset (default: all four)")
     a = ap.parse_args()
     ctx = PrefillContext(SHAPES["tiny"], kv_pages=8, max_pos=1024)
     st = torch.cuda.ExternalStream(ctx.stream_ptr)
     lib = ctx.lib
     res = []
-    for N, K in SHAPES_NK:
+    shapes = [tuple(int(v) for v in x.split(",")) for x in a.shapes.split(";")] if a.shapes else SHAPES_NK
+    for N, K in shapes:
         copies = max(2, int(400e6 // (N * K * 2)) + 1)  # > 3x L2 of weights in rotation
         Bs = [torch.randn(N, K, device="cuda", dtype=torch.bfloat16) for _ in range(copies)]
         for M in MS:
@@ -42,7 +45,8 @@ def main():
                     def call():
                         B = Bs[i[0] % copies]
                         i[0] += 1
-                        lib.fp_op_gemm(ctx.h, 2, A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K)
+                        lib.fp_op_gemm(ctx.h, EPI.get((N, K), 2), A.data_ptr(), B.data_ptr(),
+                                       C.data_ptr(), M, N, K)
 
                     for _ in range(3):
                         call()
