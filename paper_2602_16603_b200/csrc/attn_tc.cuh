@@ -189,7 +189,9 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
   uint8_t* sQ = smem;                      // [2][TILE_BYTES]
   uint8_t* sKV = smem + 2 * TILE_BYTES;    // [STAGES][TILE_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + STAGES * TILE_BYTES);
+  // [2 heads][TILE_BYTES] output staging: 1024-byte aligned (the 128B-swizzle atom the TMA reads)
+  uint8_t* sOut = sKV + STAGES * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + 2 * TILE_BYTES);
   uint64_t* q_full = bars;
   uint64_t* q_empty = bars + 1;
   uint64_t* kv_full = bars + 2;
@@ -202,7 +204,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   uint64_t* w_empty = w_full + 2;        // [2]
   int* w_ring = reinterpret_cast<int*>(w_empty + 2);  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_ring + 2);
-  uint8_t* sOut = sKV + STAGES * TILE_BYTES + 512;  // [2 heads][TILE_BYTES] output staging
 
   const int warp = warp_id();
   const int lane = lane_id();
