@@ -412,11 +412,28 @@ def run_ours(args):
     except Exception as e:  # keep the bench line; record why the leg failed
         pre = {"error": repr(e)[:300]}
 
+    # -------- the TTFT predictor the scheduler ranks with (S-EDF slack, Alg. 1 admission):
+    # fitted by the reference's own fit_ttft_poly to measured B200 single-request latencies on
+    # its log-spaced grid (`prefillsim calibrate`)
+    ttft = None
+    if rank == 0 and not args.skip_goodput:
+        try:
+            from paper_2602_16603_b200.calibrate import (fit_ttft_predictor, measure_ttft_samples,
+                                                         ttft_grid)
+
+            samples = measure_ttft_samples(ctx, shape, ttft_grid())
+            poly, quality = fit_ttft_predictor(samples, 2)
+            ttft = {"poly": poly, "samples": [[int(n), round(t, 6)] for n, t in samples],
+                    "coefficients": list(poly.coefficients), **quality}
+        except Exception as e:  # the reference is absent or the fit was rejected
+            ttft = {"error": repr(e)[:200]}
+
     # -------- goodput: reference goodput_search on the B200-calibrated cost model
     good = None
     if rank == 0 and not args.skip_goodput:
         try:
-            good = calibrated_goodput(prof, shape, args, ws)
+            good = calibrated_goodput(prof, shape, args, ws,
+                                      ttft.get("poly") if isinstance(ttft, dict) else None)
         except Exception as e:  # keep the bench line even if the reference is unavailable
             good = {"error": repr(e)[:200]}
 
@@ -426,7 +443,8 @@ def run_ours(args):
             t.destroy()
         tasks = []
         try:
-            good["live_check"] = live_check(ctx, shape, good, args)
+            good["live_check"] = live_check(ctx, shape, good, args,
+                                            ttft.get("poly") if isinstance(ttft, dict) else None)
         except Exception as e:
             good["live_check"] = {"error": repr(e)[:300]}
 
@@ -490,6 +508,8 @@ def run_ours(args):
             "p99_preempt_latency_ms": pre.get("p99_ms"),
             "preemption": pre,
             "goodput": good,
+            "ttft_predictor": ({k: v for k, v in ttft.items() if k != "poly"}
+                               if isinstance(ttft, dict) else None),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -569,7 +589,7 @@ def preemption_latency(ctx, shape, rank: int, n_signals: int = 40, length: int =
     }
 
 
-def live_run(ctx, shape, params, pc, rate, duration):
+def live_run(ctx, shape, params, pc, rate, duration):  # pc.predictor: the measured fit
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.live import replay_rounds, run_live
 
@@ -609,7 +629,7 @@ def live_run(ctx, shape, params, pc, rate, duration):
     }
 
 
-def live_check(ctx, shape, good, args):
+def live_check(ctx, shape, good, args, predictor=None):
     """Wall-clock goodput: the live driver replays `live_duration` s of the config-2 trace at
     candidate rates (bisection between 0.5x and 1x the calibrated goodput, 90% target), for
     S-EDF + operator preemption; EDF + 2048-token chunks (DistServe-CP analogue) is replayed at
@@ -618,9 +638,9 @@ def live_check(ctx, shape, good, args):
 
     ps = refsim.load()
     params = ps.CostParams.from_json_dict(good["cost_params"])
-    sedf = ps.PolicyConfig()
+    sedf = ps.PolicyConfig(predictor=predictor)
     cp2k = ps.PolicyConfig(policy=ps.PolicyKind.EDF, granularity=ps.PreemptionGranularity.CHUNK,
-                           chunk_tokens=2048)
+                           chunk_tokens=2048, predictor=predictor)
     r0 = float(good["value"])
     probes = []
     hi_run = live_run(ctx, shape, params, sedf, r0, args.live_duration)
@@ -653,7 +673,7 @@ def live_check(ctx, shape, good, args):
     }
 
 
-def calibrated_goodput(prof, shape, args, n_instances: int = 1):
+def calibrated_goodput(prof, shape, args, n_instances: int = 1, predictor=None):
     from paper_2602_16603_b200 import refsim
     from paper_2602_16603_b200.calibrate import fit_cost_params, predicted_vs_measured
 
@@ -661,7 +681,7 @@ def calibrated_goodput(prof, shape, args, n_instances: int = 1):
     params = fit_cost_params(prof, shape.num_layers)
     err = predicted_vs_measured(params, prof)
     base = config2_trace(rate=20.0, duration=args.goodput_duration)
-    rc = ps.RunConfig(ps.PolicyConfig(), params)
+    rc = ps.RunConfig(ps.PolicyConfig(predictor=predictor), params)
     t0 = time.perf_counter()
     res = ps.goodput_search(base, rc, target=0.9, rate_bounds=(1.0, 512.0), tol=0.05)
     out = {
@@ -680,7 +700,7 @@ def calibrated_goodput(prof, shape, args, n_instances: int = 1):
     try:
         rc2 = ps.RunConfig(ps.PolicyConfig(policy=ps.PolicyKind.EDF,
                                            granularity=ps.PreemptionGranularity.CHUNK,
-                                           chunk_tokens=2048), params)
+                                           chunk_tokens=2048, predictor=predictor), params)
         r2 = ps.goodput_search(base, rc2, target=0.9, rate_bounds=(1.0, 512.0), tol=0.05)
         out["edf_chunk2048_value"] = r2.value
     except Exception as e:

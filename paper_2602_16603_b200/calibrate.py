@@ -102,3 +102,47 @@ def predicted_vs_measured(params, records: Sequence[dict]) -> float:
             pred = ps.operator_duration(ps.OperatorKind(op), int(m), 0, params)
             worst = max(worst, abs(pred - y) / max(y, 1e-9))
     return worst
+
+
+def measure_ttft_samples(ctx, shape, lengths: Sequence[int], reps: int = 2) -> list:
+    """Measured single-request prefill latency (tokens, seconds) on the device: one task per
+    length, CUDA events around its whole entry list on the prefill stream, median of `reps`
+    runs after a warm-up run. The profile the reference's `prefillsim calibrate` consumes
+    (cli.py:251-267: a tokens,seconds CSV)."""
+    import torch
+
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr)
+    rng = np.random.default_rng(0)
+    out = []
+    for n in lengths:
+        task = ctx.create_task([rng.integers(0, shape.vocab, int(n)).astype(np.int32)])
+        times = []
+        for r in range(reps + 1):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            task.begin_segment(0)
+            e0.record(stream)
+            task.enqueue(0, task.n_entries)
+            e1.record(stream)
+            ctx.sync()
+            if r:
+                times.append(e0.elapsed_time(e1) * 1e-3)
+        task.destroy()
+        out.append((float(n), float(np.median(times))))
+    return out
+
+
+def fit_ttft_predictor(samples: Sequence, degree: int = 2):
+    """The reference's own predictor fit on measured latencies (`fit_ttft_poly`,
+    cost_model.py:271-301, as `prefillsim calibrate` runs it) and its `fit_quality`."""
+    refsim.load()
+    from prefillsim import cost_model as cm
+
+    poly = cm.fit_ttft_poly(list(samples), degree)
+    return poly, cm.fit_quality(list(samples), poly)
+
+
+def ttft_grid(lo: int = 64, hi: int = 32768, points: int = 17) -> list:
+    """The reference's log-spaced calibration grid (self_calibrated_poly, cost_model.py:322-343),
+    capped at the context's position table."""
+    return [int(n) for n in np.unique(np.round(np.geomspace(lo, hi, points)).astype(int))]

@@ -62,6 +62,8 @@ def run_live(
     arrivals and completions it consumes, the cursor of every live task as the scheduler saw
     it, and the commands it returned -- for ``replay_rounds`` (SURVEY.md §7 hard part 5)."""
     if predictor is None:
+        predictor = policy_config.predictor  # as the reference run() does (engine.py:399-406)
+    if predictor is None:
         predictor = ps.self_calibrated_poly(
             cost_params, degree=policy_config.predictor_degree,
             chunk_size=policy_config.chunk_tokens)
@@ -296,6 +298,8 @@ def replay_rounds(trace, policy_config, cost_params, round_log: list, predictor=
     signal running at the ACK instant; every ACK cursor an eligible boundary of the task's
     granularity (engine.py:127-134) at or after the cursor the preempting round saw.
     Returns counts; raises ``AssertionError`` on the first mismatch."""
+    if predictor is None:
+        predictor = policy_config.predictor
     if predictor is None:
         predictor = ps.self_calibrated_poly(
             cost_params, degree=policy_config.predictor_degree,
