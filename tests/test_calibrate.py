@@ -73,3 +73,22 @@ def test_fit_ignores_single_outlier_launches():
             break
     p = fit_cost_params(recs, num_layers=32)
     assert predicted_vs_measured(p, recs) <= 1e-3
+
+
+def test_ttft_predictor_is_the_reference_fit():
+    """The live predictor is the reference's own fit_ttft_poly over (tokens, seconds) samples on
+    the reference's log-spaced grid (`prefillsim calibrate`, cli.py:251-267); the wall-clock
+    driver takes it through PolicyConfig.predictor like the reference run()."""
+    from paper_2602_16603_b200.calibrate import fit_ttft_predictor, ttft_grid
+
+    ps = refsim_or_skip()
+    from prefillsim import cost_model as cm
+
+    grid = ttft_grid()
+    assert grid[0] == 64 and grid[-1] == 32768 and len(grid) == 17
+    samples = [(float(n), 2e-3 + 9e-7 * n + 3e-12 * n * n) for n in grid]
+    poly, q = fit_ttft_predictor(samples, 2)
+    ref = cm.fit_ttft_poly(samples, 2)
+    assert poly.coefficients == ref.coefficients
+    assert q["r2"] > 0.999999
+    assert isinstance(ps.PolicyConfig(predictor=poly).predictor, type(ref))
