@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   uint64_t* o_empty = o_full + 2;        // [2]
   uint64_t* w_full = o_empty + 2;        // [2] work ring
   uint64_t* w_empty = w_full + 2;        // [2]
-  int* w_ring = reinterpret_cast<int*>(w_empty + 2);  // [2]
+  uint64_t* p_half = w_empty + 2;        // [2] per head: P of kv columns 0-63 in TMEM
+  int* w_ring = reinterpret_cast<int*>(p_half + 2);  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_ring + 2);
 
   const int warp = warp_id();
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     for (int h = 0; h < 2; ++h) {
       mbar_init(&s_full[h], 1);
       mbar_init(&p_full[h], 128);
+      mbar_init(&p_half[h], 128);
       mbar_init(&o_empty[h], 128);
       mbar_init(&o_full[h], 1);
       mbar_init(&w_full[h], 1);
@@ -314,11 +316,11 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         umma_bf16_ss(tS[h], qdesc[h] + off, kd + off, idesc_qk, kk > 0);
       }
     };
-    auto issue_pv = [&](int h, uint32_t vsq, bool acc) {
+    auto issue_pv = [&](int h, uint32_t vsq, bool acc, int k_lo = 0, int k_hi = 8) {
       const uint64_t vd =
           make_sdesc_sw128(smem_u32(sKV + slot_of(vsq) * TILE_BYTES), ATOM_BYTES, 1024);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {  // 128 kv rows = 8 x K16; P: 8 TMEM columns per step
+      for (int kk = k_lo; kk < k_hi; ++kk) {  // 128 kv rows = 8 x K16; P: 8 TMEM columns per step
         umma_bf16_ts(tO[h], tS[h] + kk * 8, vd + (uint64_t)((kk * 2048) >> 4), idesc_pv,
                      (acc || kk > 0) ? 1u : 0u);
       }
@@ -357,14 +359,30 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         const uint32_t ksq = seq + 1;  // K_{j+1}
         const uint32_t tph = (tc + j) & 1;
         wait_tile(vsq);
-        mbar_wait(&p_full[0], tph);
         if (j == 0) mbar_wait(&o_empty[0], (it & 1) ^ 1);  // previous item's O0 drained
+#ifdef FP_ATTN_SPLIT_P
+        // P*V on kv rows 0-63 as soon as that half of P is in TMEM: it overlaps the softmax's
+        // second half of exponentials
+        mbar_wait(&p_half[0], tph);
+        tc_fence_after();
+        if (lane == 0) issue_pv(0, vsq, j > 0, 0, 4);
+        __syncwarp();
+        mbar_wait(&p_full[0], tph);
+        tc_fence_after();
+        if (lane == 0) ATTN_STAMP(it, j, 4);
+        if (lane == 0) {
+          issue_pv(0, vsq, true, 4, 8);
+          if (last) tc_commit(&o_full[0]);  // head 0's epilogue need not wait for head 1
+        }
+#else
+        mbar_wait(&p_full[0], tph);
         tc_fence_after();
         if (lane == 0) ATTN_STAMP(it, j, 4);
         if (lane == 0) {
           issue_pv(0, vsq, j > 0);
           if (last) tc_commit(&o_full[0]);  // head 0's epilogue need not wait for head 1
         }
+#endif
         __syncwarp();
         if (!last) {
           wait_tile(ksq);
@@ -377,12 +395,24 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           }
           __syncwarp();
         }
-        mbar_wait(&p_full[1], tph);
         if (j == 0) mbar_wait(&o_empty[1], (it & 1) ^ 1);
+#ifdef FP_ATTN_SPLIT_P
+        mbar_wait(&p_half[1], tph);
+        tc_fence_after();
+        if (lane == 0) issue_pv(1, vsq, j > 0, 0, 4);
+        __syncwarp();
+        mbar_wait(&p_full[1], tph);
+        tc_fence_after();
+        if (lane == 0) ATTN_STAMP(it, j, 6);
+        if (lane == 0) {
+          issue_pv(1, vsq, true, 4, 8);
+#else
+        mbar_wait(&p_full[1], tph);
         tc_fence_after();
         if (lane == 0) ATTN_STAMP(it, j, 6);
         if (lane == 0) {
           issue_pv(1, vsq, j > 0);
+#endif
           if (last) tc_commit(&o_full[1]);
           tc_commit(&kv_empty[slot_of(vsq)]);
           if (!last) {
@@ -503,6 +533,13 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
             pk[i >> 1] = pack_bf16x2(e.x, e.y);
           }
           tmem_st16(tS + c * 16, pk);  // P (bf16 pairs) over the consumed S columns
+#ifdef FP_ATTN_SPLIT_P
+          if (c == 1) {  // kv columns 0-63 of P are in TMEM: the first half of P*V may run
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_half[h]);
+          }
+#endif
         }
         if (row == 0) ATTN_STAMP(it, j, 12 + 4 * h);
         tmem_st_wait();
