@@ -64,7 +64,7 @@ def main():
     from paper_2602_16603_b200 import dispatch, refsim
     from paper_2602_16603_b200.calibrate import fit_cost_params, predicted_vs_measured
     from paper_2602_16603_b200.config import SHAPES
-    from paper_2602_16603_b200.live import run_live
+    from paper_2602_16603_b200.live import replay_rounds, run_live
     from paper_2602_16603_b200.native import PrefillContext
 
     ps = refsim.load()
@@ -108,8 +108,16 @@ def main():
         for rate in [float(x) for x in a.rates.split(",")]:
             tr = ps.generate_trace(classes, rate, a.duration, 5)
             t0 = time.perf_counter()
-            res = run_live(tr, pc, params, ctx, tok, max_wall_s=10 * a.duration + 120)
+            rounds: list = []
+            res = run_live(tr, pc, params, ctx, tok, max_wall_s=10 * a.duration + 120,
+                           round_log=rounds)
             bl = ps.blocking_stats(res.blocking_log)
+            try:  # wall-clock scheduling parity: every round through a fresh reference scheduler
+                rep = replay_rounds(tr, pc, params, rounds)
+                replay = {"rounds": rep["rounds"], "mismatches": 0}
+            except AssertionError as e:
+                replay = {"mismatch": str(e)[:200]}
+            max_entry = {r["done"]: r["max_entry_s"] for r in rounds if "done" in r}
             rows.append({
                 "rate_req_s": rate,
                 "requests": len(tr),
@@ -120,6 +128,8 @@ def main():
                 "p99_blocking_ms": None if bl["p99_s"] is None else round(bl["p99_s"] * 1e3, 3),
                 "max_blocking_ms": None if bl["max_s"] is None else round(bl["max_s"] * 1e3, 3),
                 "wall_s": round(time.perf_counter() - t0, 2),
+                "replay": replay,
+                "longest_entry_ms": round(max(max_entry.values()) * 1e3, 3) if max_entry else None,
             })
             print(name, rows[-1], flush=True)
         live[name] = rows
