@@ -494,7 +494,10 @@ def run_ours(args):
                 "peak_source": f"{peak_kind} bf16_tflops_sustained (kernels timed inside a long step)",
                 "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4) if peak else None,
-                "traffic": traffic,
+                # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full of the
+                # same kernel at M = 4465), and where it came from
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic_detail": traffic,
                 "all_dense_gemms_tflops": round(all_gemm, 1),
             },
             "kernels": kernels,

@@ -54,6 +54,7 @@ def test_our_arm_json_line():
     r = d["roofline"]
     assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and 0 < r["frac"] <= 1.2
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert r["traffic"] is None or isinstance(r["traffic"], (int, float))  # bytes per launch
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["gpu_launches"] > 0
     c = d["clocks"]
