@@ -330,7 +330,9 @@ static constexpr double kSplitOverheadKb = 44.0;
 static constexpr double kSplitOverheadKbQkv = 60.0;  // RoPE / KV-scatter items cost more
 // Tails behind full waves split only for long K (down_proj): the split-capable instantiation
 // runs the full-wave tiles with more register pressure (measured slower for QKV / SwiGLU).
+static int g_split_tail = 0;  // FP_SPLIT_TAIL=1 (experiments): tail split for every epilogue / K
 static bool split_tail_ok(int epi, int K) {
+  if (g_split_tail) return epi != EPI_STORE_F32;
   return epi != EPI_QKV && epi != EPI_SWIGLU && epi != EPI_STORE_F32 && K / kGemmBK >= 128;
 }
 static double g_split_ov_scale = 1.0;  // FP_SPLIT_OV_SCALE (experiments)
@@ -1124,6 +1126,7 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
     if (const char* e = getenv("FP_RASTER_ALL_MB")) g_raster_all_mb = atoi(e);
     if (const char* e = getenv("FP_SK_FIX_SCALE")) g_sk_fix_scale = atof(e);
     if (const char* e = getenv("FP_SPLIT_OV_SCALE")) g_split_ov_scale = atof(e);
+    if (const char* e = getenv("FP_SPLIT_TAIL")) g_split_tail = atoi(e);
     if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
     if (const char* e = getenv("FP_TP_FUSED")) c->tp_fused = atoi(e) != 0;
