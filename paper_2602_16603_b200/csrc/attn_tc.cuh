@@ -472,6 +472,76 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           for (int i = 0; i < 128; ++i)
             if (kv0 + i > qpos) sr[i] = -INFINITY;
         }
+#ifdef FP_ATTN_SPEC_MAX
+        if (j > 0) {
+          // Speculative P: the exponentials use the running max m while the row max is still
+          // being computed (the lazy rescale keeps m unless the max grew by > 2^8, so this is
+          // the final P in the common case, bit for bit); a row whose max grew past that
+          // recomputes its P after the O rescale, before P is released.
+          auto exp_store = [&](float nm, float2& acc0, float2& acc1) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const float2 x = ffma2(make_float2(sr[c * 32 + i], sr[c * 32 + i + 1]),
+                                       make_float2(sc, sc), make_float2(nm, nm));
+                float2 e;
+                if (((i & 15) >> 1) < FP_ATTN_EMU) {
+                  e = exp2_poly2(x);
+                } else {
+                  e.x = fast_exp2(x.x);
+                  e.y = fast_exp2(x.y);
+                }
+                if (i & 2) acc1 = fadd2(acc1, e);
+                else acc0 = fadd2(acc0, e);
+                pk[i >> 1] = pack_bf16x2(e.x, e.y);
+              }
+              tmem_st16(tS + c * 16, pk);
+            }
+          };
+          float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+          exp_store((m == -INFINITY) ? 0.f : -m, acc0, acc1);
+          float mc[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mc[k] = fmaxf(sr[k], sr[8 + k]);
+#pragma unroll
+          for (int i = 16; i < 128; i += 16) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mc[k] = fmaxf(mc[k], fmaxf(sr[i + k], sr[i + 8 + k]));
+          }
+          const float mx = fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])),
+                                 fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7])));
+          const float m_new = fmaxf(m, mx * sc);
+          const bool need = m_new > m + RESCALE_THRESHOLD;
+          if (__any_sync(0xffffffffu, need)) {
+            const float alpha = need ? fast_exp2(m - m_new) : 1.f;
+            if (need) {
+              l *= alpha;
+              m = m_new;
+            }
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld32(tO + c * 32, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(tO + c * 32, o);
+            }
+            tmem_st_wait();
+            acc0 = make_float2(0.f, 0.f);  // every row redoes its P (unchanged rows: same bits)
+            acc1 = make_float2(0.f, 0.f);
+            exp_store((m == -INFINITY) ? 0.f : -m, acc0, acc1);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&p_full[h]);
+          if (row == 0 && h == 0 && j == a.n_tiles - 1) ATTN_ISTAMP(it, 3);
+          l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
+          continue;
+        }
+#endif
 #ifndef FP_ATTN_CHAIN_MAX
         // 8 independent 3-input max chains, then a 3-level tree (latency ~ 16 dependent ops)
         float mc[8];
