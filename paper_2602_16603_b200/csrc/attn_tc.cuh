@@ -202,8 +202,7 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
   uint64_t* o_empty = o_full + 2;        // [2]
   uint64_t* w_full = o_empty + 2;        // [2] work ring
   uint64_t* w_empty = w_full + 2;        // [2]
-  uint64_t* p_half = w_empty + 2;        // [2] per head: P of kv columns 0-63 in TMEM
-  int* w_ring = reinterpret_cast<int*>(p_half + 2);  // [2]
+  int* w_ring = reinterpret_cast<int*>(w_empty + 2);  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_ring + 2);
 
   const int warp = warp_id();
@@ -221,7 +220,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
     for (int h = 0; h < 2; ++h) {
       mbar_init(&s_full[h], 1);
       mbar_init(&p_full[h], 128);
-      mbar_init(&p_half[h], 128);
       mbar_init(&o_empty[h], 128);
       mbar_init(&o_full[h], 1);
       mbar_init(&w_full[h], 1);
@@ -316,11 +314,11 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         umma_bf16_ss(tS[h], qdesc[h] + off, kd + off, idesc_qk, kk > 0);
       }
     };
-    auto issue_pv = [&](int h, uint32_t vsq, bool acc, int k_lo = 0, int k_hi = 8) {
+    auto issue_pv = [&](int h, uint32_t vsq, bool acc) {
       const uint64_t vd =
           make_sdesc_sw128(smem_u32(sKV + slot_of(vsq) * TILE_BYTES), ATOM_BYTES, 1024);
 #pragma unroll
-      for (int kk = k_lo; kk < k_hi; ++kk) {  // 128 kv rows = 8 x K16; P: 8 TMEM columns per step
+      for (int kk = 0; kk < 8; ++kk) {  // 128 kv rows = 8 x K16; P: 8 TMEM columns per step
         umma_bf16_ts(tO[h], tS[h] + kk * 8, vd + (uint64_t)((kk * 2048) >> 4), idesc_pv,
                      (acc || kk > 0) ? 1u : 0u);
       }
@@ -360,21 +358,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
         const uint32_t tph = (tc + j) & 1;
         wait_tile(vsq);
         if (j == 0) mbar_wait(&o_empty[0], (it & 1) ^ 1);  // previous item's O0 drained
-#ifdef FP_ATTN_SPLIT_P
-        // P*V on kv rows 0-63 as soon as that half of P is in TMEM: it overlaps the softmax's
-        // second half of exponentials
-        mbar_wait(&p_half[0], tph);
-        tc_fence_after();
-        if (lane == 0) issue_pv(0, vsq, j > 0, 0, 4);
-        __syncwarp();
-        mbar_wait(&p_full[0], tph);
-        tc_fence_after();
-        if (lane == 0) ATTN_STAMP(it, j, 4);
-        if (lane == 0) {
-          issue_pv(0, vsq, true, 4, 8);
-          if (last) tc_commit(&o_full[0]);  // head 0's epilogue need not wait for head 1
-        }
-#else
         mbar_wait(&p_full[0], tph);
         tc_fence_after();
         if (lane == 0) ATTN_STAMP(it, j, 4);
@@ -382,7 +365,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           issue_pv(0, vsq, j > 0);
           if (last) tc_commit(&o_full[0]);  // head 0's epilogue need not wait for head 1
         }
-#endif
         __syncwarp();
         if (!last) {
           wait_tile(ksq);
@@ -396,23 +378,11 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           __syncwarp();
         }
         if (j == 0) mbar_wait(&o_empty[1], (it & 1) ^ 1);
-#ifdef FP_ATTN_SPLIT_P
-        mbar_wait(&p_half[1], tph);
-        tc_fence_after();
-        if (lane == 0) issue_pv(1, vsq, j > 0, 0, 4);
-        __syncwarp();
-        mbar_wait(&p_full[1], tph);
-        tc_fence_after();
-        if (lane == 0) ATTN_STAMP(it, j, 6);
-        if (lane == 0) {
-          issue_pv(1, vsq, true, 4, 8);
-#else
         mbar_wait(&p_full[1], tph);
         tc_fence_after();
         if (lane == 0) ATTN_STAMP(it, j, 6);
         if (lane == 0) {
           issue_pv(1, vsq, j > 0);
-#endif
           if (last) tc_commit(&o_full[1]);
           tc_commit(&kv_empty[slot_of(vsq)]);
           if (!last) {
@@ -472,76 +442,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
           for (int i = 0; i < 128; ++i)
             if (kv0 + i > qpos) sr[i] = -INFINITY;
         }
-#ifdef FP_ATTN_SPEC_MAX
-        if (j > 0) {
-          // Speculative P: the exponentials use the running max m while the row max is still
-          // being computed (the lazy rescale keeps m unless the max grew by > 2^8, so this is
-          // the final P in the common case, bit for bit); a row whose max grew past that
-          // recomputes its P after the O rescale, before P is released.
-          auto exp_store = [&](float nm, float2& acc0, float2& acc1) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t pk[16];
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                const float2 x = ffma2(make_float2(sr[c * 32 + i], sr[c * 32 + i + 1]),
-                                       make_float2(sc, sc), make_float2(nm, nm));
-                float2 e;
-                if (((i & 15) >> 1) < FP_ATTN_EMU) {
-                  e = exp2_poly2(x);
-                } else {
-                  e.x = fast_exp2(x.x);
-                  e.y = fast_exp2(x.y);
-                }
-                if (i & 2) acc1 = fadd2(acc1, e);
-                else acc0 = fadd2(acc0, e);
-                pk[i >> 1] = pack_bf16x2(e.x, e.y);
-              }
-              tmem_st16(tS + c * 16, pk);
-            }
-          };
-          float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-          exp_store((m == -INFINITY) ? 0.f : -m, acc0, acc1);
-          float mc[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mc[k] = fmaxf(sr[k], sr[8 + k]);
-#pragma unroll
-          for (int i = 16; i < 128; i += 16) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) mc[k] = fmaxf(mc[k], fmaxf(sr[i + k], sr[i + 8 + k]));
-          }
-          const float mx = fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])),
-                                 fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7])));
-          const float m_new = fmaxf(m, mx * sc);
-          const bool need = m_new > m + RESCALE_THRESHOLD;
-          if (__any_sync(0xffffffffu, need)) {
-            const float alpha = need ? fast_exp2(m - m_new) : 1.f;
-            if (need) {
-              l *= alpha;
-              m = m_new;
-            }
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-              uint32_t o[32];
-              tmem_ld32(tO + c * 32, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st32(tO + c * 32, o);
-            }
-            tmem_st_wait();
-            acc0 = make_float2(0.f, 0.f);  // every row redoes its P (unchanged rows: same bits)
-            acc1 = make_float2(0.f, 0.f);
-            exp_store((m == -INFINITY) ? 0.f : -m, acc0, acc1);
-          }
-          tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(&p_full[h]);
-          if (row == 0 && h == 0 && j == a.n_tiles - 1) ATTN_ISTAMP(it, 3);
-          l += (acc0.x + acc0.y) + (acc1.x + acc1.y);
-          continue;
-        }
-#endif
 #ifndef FP_ATTN_CHAIN_MAX
         // 8 independent 3-input max chains, then a 3-level tree (latency ~ 16 dependent ops)
         float mc[8];
@@ -603,13 +503,6 @@ __global__ void __launch_bounds__(tcattn::THREADS, 1)
             pk[i >> 1] = pack_bf16x2(e.x, e.y);
           }
           tmem_st16(tS + c * 16, pk);  // P (bf16 pairs) over the consumed S columns
-#ifdef FP_ATTN_SPLIT_P
-          if (c == 1) {  // kv columns 0-63 of P are in TMEM: the first half of P*V may run
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&p_half[h]);
-          }
-#endif
         }
         if (row == 0) ATTN_STAMP(it, j, 12 + 4 * h);
         tmem_st_wait();
