@@ -21,7 +21,9 @@
 //                issued ping-pong so head 1's MMAs overlap head 0's softmax and vice versa
 //   warps 2-5    softmax for head 0, warps 6-9 softmax for head 1: one query row per thread,
 //                exp2 online softmax with lazy O rescale (only when the row max grows by > 2^8),
-//                P written back to TMEM over S as bf16, final O / l epilogue to HBM.
+//                P written back to TMEM over S as bf16; per-head O-complete barrier, then the
+//                O / l epilogue: full query tiles staged in 128B-swizzled shared memory and
+//                written by TMA stores (coalesced), a request's partial last tile row by row.
 // Softmax arithmetic is budgeted against the tensor pipe: the scale is folded into one packed
 // FFMA2 per element pair, the row max is a tree of 8 chains, row sums use packed FADD2 after P
 // is released, and 2 of every 8 exponential pairs run as a degree-3 polynomial on the FMA pipe
