@@ -18,6 +18,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--model", default="llama3-8b")
+    ap.add_argument("--granularity", default="operator",
+                    help="none: no boundary is eligible, so no kernel reads the host flag")
     a = ap.parse_args()
     import torch
 
@@ -29,7 +31,8 @@ def main():
                          page_size=128, max_pos=8192)
     ctx.init_random(seed=0)
     st = torch.cuda.ExternalStream(ctx.stream_ptr)
-    tasks = [ctx.create_task([np.random.default_rng(i).integers(0, shape.vocab, n).astype(np.int32)])
+    tasks = [ctx.create_task([np.random.default_rng(i).integers(0, shape.vocab, n).astype(np.int32)],
+                             None, a.granularity)
              for i, n in enumerate(LENS)]
 
     def step():
