@@ -274,10 +274,15 @@ int fp_op_attn_prefill(fp_ctx* ctx, const void* q, const void* k, const void* v,
                        int32_t n_q, int32_t kv_len);
 /* GEMM tiling override for experiments and split-K parity tests: pair = -1 auto, 0 single-CTA
  * tiles, 1 CTA-pair tiles, 2 narrow 128 x 128 tiles (residual / QKV epilogues), 3 stream-K
- * (whole tiles, then equal (tile, k-block) ranges per CTA); splits = 0
+ * (whole tiles, then equal (tile, k-block) ranges per CTA), 4 swap-AB skinny (M <= 256: weight
+ * rows as the MMA M dimension, equal weight ranges per CTA); splits = 0
  * auto, S >= 1 forces S K-slices on the partial-wave tiles (clamped so the split units fit one
  * round of the persistent grid). */
 int fp_ctx_set_gemm_policy(fp_ctx* ctx, int32_t pair, int32_t splits);
+/* Largest launch M (tokens) planned with the swap-AB skinny GEMM under the auto policy
+ * (default 128, also FP_SKINNY_MAX_M at fp_ctx_create; 0 disables it). Below it the auto policy
+ * takes the skinny plan for M <= 8, and for K >= 8192 (down_proj) up to this M. */
+int fp_ctx_set_skinny_max(fp_ctx* ctx, int32_t max_m);
 /* Batch-invariant numerics (also FP_BATCH_INVARIANT=1 at fp_ctx_create): no split-K and no
  * stream-K, so each output element is one in-order accumulation over K whatever the launch's
  * M, and a request's logits / KV are bit-identical alone or in any batch (SURVEY.md §7 hard

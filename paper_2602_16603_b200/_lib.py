@@ -123,6 +123,7 @@ _SIGS = {
     "fp_ctx_free_pages": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "fp_ctx_set_window": (C.c_int, [_P, _I]),
     "fp_ctx_set_gemm_policy": (C.c_int, [_P, _I, _I]),
+    "fp_ctx_set_skinny_max": (C.c_int, [_P, _I]),
     "fp_ctx_set_batch_invariant": (C.c_int, [_P, _I]),
     "fp_task_read_routing": (C.c_int, [_P, _P, _P, _P, _I]),
     "fp_op_gate_up_swiglu": (C.c_int, [_P, _P, _P, _P, _P, _I, _I, _I]),

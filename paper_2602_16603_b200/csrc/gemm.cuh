@@ -310,8 +310,8 @@ DEVI void tp_fold_tile(const GemmParams& p, const TpDev* tp, int slot, unsigned 
 //                            and their RoPE partners [64 + 16q, 64 + 16q + 16)
 // EPI_RESID writes the row's sum of squares (8 chunk sums in chunk order) to ssq_out; the Qwen3
 // q/k-norm sums a head's 4 items in quarter order.
-template <int EPI>
-__device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const GmemSum& sum,
+template <int EPI, class Sum = GmemSum>
+__device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const Sum& sum,
                                                  bool valid, int m, int r, int g, int n0,
                                                  int nb) {
   constexpr int BN = 256;
@@ -393,7 +393,7 @@ __device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const G
     const float* hn = is_v ? nullptr : (is_q ? p.q_norm : p.k_norm);
     float ss = 0.f;
     if (live) {
-      sum.get<2>(r, hh * 128 + q * 16, hh * 128 + 64 + q * 16, v);  // ILP 2: register budget
+      sum.template get<2>(r, hh * 128 + q * 16, hh * 128 + 64 + q * 16, v);  // ILP 2: register budget
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= rs;
       if (bias) {

@@ -20,6 +20,7 @@
 #include "gemm.cuh"
 #include "moe.cuh"
 #include "norm.cuh"
+#include "skinny.cuh"
 #include "xchg.cuh"
 
 using namespace fp;
@@ -153,6 +154,7 @@ struct Task {
   TaskCtl* ctl;
   unsigned long long* stamps = nullptr;  // inside the ctl allocation
   CUtensorMap tm_h, tm_ao, tm_act, tm_xf, tm_q;
+  CUtensorMap tm_h32, tm_ao32, tm_act32, tm_xf32;  // 32-row boxes: swap-AB skinny GEMM tokens
   // MoE routing state of the current chunk (gate -> experts) and expert-ordered buffers
   float* rlog = nullptr;                       // [max_m, 256] router logits
   char* moe_meta = nullptr;                    // one allocation for the index arrays below
@@ -243,6 +245,9 @@ struct fp_ctx {
   // (SURVEY.md §7 hard part 7). Costs the short-request speed-up of split-K.
   bool batch_invariant = false;
   int* sk_flags = nullptr;  // stream-K partial flags [num_sms]
+  // Swap-AB skinny GEMM (skinny.cuh) for launches of at most skinny_max_m tokens
+  // (FP_SKINNY_MAX_M / fp_ctx_set_skinny_max; 0 disables)
+  int skinny_max_m = 128;
   int sk_epoch = 0;         // per stream-K launch (flags compare against it: no reset)
 };
 
@@ -567,9 +572,56 @@ static double plan_cost_tiled(const fp_ctx* c, int epi, int M, int N, int K) {
   return t;
 }
 
+// Swap-AB skinny plan (skinny.cuh) for short launches: the weights stream once through all
+// SMs, one equal contiguous (128-row weight slice, k-block) range per CTA. Needs the token
+// operand's 32-row-box map; not for the TP exchange GEMMs (per-tile publish) nor batch-invariant
+// mode (its per-CTA K ranges depend on the launch shape like split-K).
+static constexpr int kSkinnySmallM = 8;     // skinny for any K up to this many rows
+static constexpr int kSkinnyLongK = 8192;   // ... and up to skinny_max_m rows from this K
+template <int EPI, int TOKMAX>
+static void launch_skinny_t(fp_ctx* c, const CUtensorMap& x32, const CUtensorMap& w,
+                            const GemmParams& p, int grid, cudaStream_t st) {
+  using Cfg = SkinnyCfg<TOKMAX>;
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, c->device, [] {
+    cudaFuncSetAttribute(gemm_skinny_kernel<EPI, TOKMAX>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  });
+  launch_pdl(gemm_skinny_kernel<EPI, TOKMAX>, dim3(grid), dim3(kGemmThreads), Cfg::SMEM_BYTES,
+             st, x32, w, p);
+}
+template <int EPI>
+static bool launch_gemm_skinny(fp_ctx* c, const CUtensorMap* x32, const CUtensorMap& w,
+                               GemmParams p, cudaStream_t st) {
+  // (TP lock-step ranks share one device: a grid-wide arrival must not compete with a peer's)
+  if (x32 == nullptr || p.xchg || c->batch_invariant || c->ws == nullptr || c->tp_lockstep)
+    return false;
+  const bool forced = c->force_pair == 4;
+  if (!forced && (c->force_pair >= 0 || c->force_splits > 0 || p.M > c->skinny_max_m))
+    return false;
+  // Auto rule from the B200 A/B (tools/skinny_ab.py, profiles/r2_skinny_ab.log): the skinny
+  // plan wins at a few rows (M = 1: qkv 1.5x, gate_up 1.46x, lm_head 1.24x) and on long-K
+  // launches up to 128 rows (down_proj 1.05-1.09x); elsewhere the tiled plans' split-K / narrow
+  // tiles are as fast or faster (both sit on the same ~10 us per-launch floor).
+  if (!forced && p.M > kSkinnySmallM && p.K < kSkinnyLongK) return false;
+  if (p.M < 1 || p.M > kSkinnyMaxM || p.N % 256 != 0 || p.K % kGemmBK != 0)
+    return false;
+  const long long U = (long long)(p.N / 128) * (p.K / kGemmBK);
+  const int grid = (int)std::max(1LL, std::min<long long>(c->num_sms, U / 4));  // >= 4 k-blocks
+  const long long ws_floats = 8LL * c->num_sms * kGemmBM * 256;
+  if ((long long)(grid + p.N / 128) * p.M * 128 > ws_floats) return false;
+  p.ws = c->ws;
+  p.tickets = c->tickets;
+  if (p.M <= 64) launch_skinny_t<EPI, 64>(c, *x32, w, p, grid, st);
+  else if (p.M <= 128) launch_skinny_t<EPI, 128>(c, *x32, w, p, grid, st);
+  else launch_skinny_t<EPI, 256>(c, *x32, w, p, grid, st);
+  return true;
+}
+
 template <int EPI>
 static void launch_gemm(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b,
-                        const GemmParams& p, cudaStream_t st) {
+                        const GemmParams& p, cudaStream_t st, const CUtensorMap* a32 = nullptr) {
+  if (launch_gemm_skinny<EPI>(c, a32, b, p, st)) return;
   if (!p.xchg && !c->batch_invariant &&
       (c->force_pair == 3 || (c->use_streamk && c->force_pair < 0 && c->force_splits == 0))) {
     const SkPlan pl = plan_streamk(c, p.M, p.N, p.K);
@@ -657,7 +709,7 @@ static int launch_final(fp_ctx* c, Task* t, const ChunkPlan& ch, int layer, cons
   q.ldo = c->vocab_pad;
   q.guard = g2;
   ProfScope ps(c, st, FP_K_LM_HEAD, layer, ch.n_last, 2.0 * ch.n_last * q.N * q.K, 0.0);
-  launch_gemm<EPI_STORE_F32>(c, t->tm_xf, c->tm_lm, q, st);
+  launch_gemm<EPI_STORE_F32>(c, t->tm_xf, c->tm_lm, q, st, &t->tm_xf32);
   return FP_OK;
 }
 
@@ -842,13 +894,13 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
       p.k_norm = ly.k_norm;
       p.norm_eps = m.rms_eps;
       ProfScope ps(c, st, FP_K_QKV, layer, M, 2.0 * M * p.N * p.K, 0.0);
-      launch_gemm<EPI_QKV>(c, t->tm_h, ly.tm_qkv, p, st);
+      launch_gemm<EPI_QKV>(c, t->tm_h, ly.tm_qkv, p, st, &t->tm_h32);
     } else {
       p.N = 2 * c->ffn;
       p.out = t->act;
       p.ldo = c->ffn;
       ProfScope ps(c, st, FP_K_GATE_UP, layer, M, 2.0 * M * p.N * p.K, 0.0);
-      launch_gemm<EPI_SWIGLU>(c, t->tm_h, ly.tm_gu, p, st);
+      launch_gemm<EPI_SWIGLU>(c, t->tm_h, ly.tm_gu, p, st, &t->tm_h32);
     }
   } else if (op == FP_OP_ATTN) {
     AttnTcParams a{};
@@ -883,10 +935,11 @@ static int launch_entry(fp_ctx* c, Task* t, int e, int phase = kPhaseAll) {
     p.K = op == FP_OP_O_PROJ ? c->qdim : c->ffn;
     const CUtensorMap& ta = op == FP_OP_O_PROJ ? t->tm_ao : t->tm_act;
     const CUtensorMap& tb = op == FP_OP_O_PROJ ? ly.tm_o : ly.tm_d;
+    const CUtensorMap* ta32 = op == FP_OP_O_PROJ ? &t->tm_ao32 : &t->tm_act32;
     const int kind = op == FP_OP_O_PROJ ? FP_K_O : FP_K_DOWN;
     if (!xchg_op) {
       ProfScope ps(c, st, kind, layer, M, 2.0 * M * p.N * p.K, 0.0);
-      launch_gemm<EPI_RESID>(c, ta, tb, p, st);
+      launch_gemm<EPI_RESID>(c, ta, tb, p, st, ta32);
     } else {
       // One process per GPU: the exchange is FUSED into the GEMM (each tile's partial is
       // flagged to the peers and folded tile by tile over NVLink inside the same kernel).
@@ -1130,6 +1183,7 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
     if (const char* e = getenv("FP_FORCE_SPLITS")) c->force_splits = atoi(e);
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
     if (const char* e = getenv("FP_TP_FUSED")) c->tp_fused = atoi(e) != 0;
+    if (const char* e = getenv("FP_SKINNY_MAX_M")) c->skinny_max_m = atoi(e);
     if (const char* e = getenv("FP_GEMM_STAMPS"))
       if (atoi(e)) CK(cudaMalloc(&c->gemm_dbg, (size_t)4096 * 16 * sizeof(unsigned long long)));
     const uint64_t rows = (uint64_t)L * kv_pages * 2 * c->hkv * page_size;
@@ -1261,9 +1315,14 @@ int fp_debug_gemm_stamps(fp_ctx* c, uint64_t* out, int32_t max_ctas) {
   return FP_OK;
 }
 int fp_ctx_set_gemm_policy(fp_ctx* c, int32_t pair, int32_t splits) {
-  REQ(c && pair >= -1 && pair <= 3 && splits >= 0 && splits <= 32, "bad gemm policy");
+  REQ(c && pair >= -1 && pair <= 4 && splits >= 0 && splits <= 32, "bad gemm policy");
   c->force_pair = pair;
   c->force_splits = splits;
+  return FP_OK;
+}
+int fp_ctx_set_skinny_max(fp_ctx* c, int32_t max_m) {
+  REQ(c && max_m >= 0, "bad skinny threshold");
+  c->skinny_max_m = max_m;
   return FP_OK;
 }
 int fp_ctx_set_batch_invariant(fp_ctx* c, int32_t on) {
@@ -1682,8 +1741,11 @@ static int task_create_impl(fp_ctx* c, const int32_t* ids, const int32_t* lens, 
   int rc;
   if ((rc = make_map(&t->tm_h, t->h, M, d, 128))) return rc;
   if ((rc = make_map(&t->tm_ao, t->ao, M, c->qdim, 128))) return rc;
+  if ((rc = make_map(&t->tm_h32, t->h, M, d, 32))) return rc;
+  if ((rc = make_map(&t->tm_ao32, t->ao, M, c->qdim, 32))) return rc;
   if (m.n_experts == 0) {
     if ((rc = make_map(&t->tm_act, t->act, M, c->ffn, 128))) return rc;
+    if ((rc = make_map(&t->tm_act32, t->act, M, c->ffn, 32))) return rc;
   } else {
     // MoE: router logits, routing index arrays (one allocation, zeroed: the histogram and the
     // scatter cursors must start at 0), expert-ordered rows
@@ -1719,6 +1781,7 @@ static int task_create_impl(fp_ctx* c, const int32_t* ids, const int32_t* lens, 
     if ((rc = make_map(&t->tm_actp, t->actp, R, I, 128))) return rc;
   }
   if ((rc = make_map(&t->tm_xf, t->xf, n_seqs, d, 128))) return rc;
+  if ((rc = make_map(&t->tm_xf32, t->xf, n_seqs, d, 32))) return rc;
   if ((rc = make_map(&t->tm_q, t->q, M, c->qdim, 128))) return rc;
   CK(cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming));
   CK(cudaEventRecord(t->ready, up));
@@ -2052,7 +2115,9 @@ int fp_op_gemm(fp_ctx* c, int32_t epi, const void* A, const void* B, void* C, in
   CK(cudaSetDevice(c->device));
   CUtensorMap ta, tb;
   int rc;
+  CUtensorMap ta32;
   if ((rc = make_map(&ta, A, M, K, 128))) return rc;
+  if ((rc = make_map(&ta32, A, M, K, 32))) return rc;
   if ((rc = make_map(&tb, B, N, K, 128))) return rc;
   GemmParams p{};
   p.M = M;
@@ -2067,12 +2132,12 @@ int fp_op_gemm(fp_ctx* c, int32_t epi, const void* A, const void* B, void* C, in
     CK(cudaMemsetAsync(c->gemm_dbg, 0, (size_t)4096 * 16 * sizeof(unsigned long long), c->stream));
     p.dbg = c->gemm_dbg;
   }
-  if (epi == 0) launch_gemm<EPI_STORE_BF16>(c, ta, tb, p, c->stream);
-  else if (epi == 1) launch_gemm<EPI_STORE_F32>(c, ta, tb, p, c->stream);
-  else if (epi == 2) launch_gemm<EPI_RESID>(c, ta, tb, p, c->stream);
+  if (epi == 0) launch_gemm<EPI_STORE_BF16>(c, ta, tb, p, c->stream, &ta32);
+  else if (epi == 1) launch_gemm<EPI_STORE_F32>(c, ta, tb, p, c->stream, &ta32);
+  else if (epi == 2) launch_gemm<EPI_RESID>(c, ta, tb, p, c->stream, &ta32);
   else if (epi == 3) {  // SwiGLU over B already packed [gate(128) | up(128)] per 256 rows
     p.ldo = N / 2;
-    launch_gemm<EPI_SWIGLU>(c, ta, tb, p, c->stream);
+    launch_gemm<EPI_SWIGLU>(c, ta, tb, p, c->stream, &ta32);
   } else return set_err(FP_ERR_ARG, "bad epilogue");
   CK(cudaGetLastError());
   return FP_OK;
@@ -2093,7 +2158,9 @@ int fp_op_gate_up_swiglu(fp_ctx* c, const void* x, const void* w_gate, const voi
                          cudaMemcpyDeviceToDevice, c->stream));
   CUtensorMap ta, tb;
   int rc;
-  if ((rc = make_map(&ta, x, M, K, 128)) || (rc = make_map(&tb, w, 2 * F, K, 128))) {
+  CUtensorMap ta32;
+  if ((rc = make_map(&ta, x, M, K, 128)) || (rc = make_map(&ta32, x, M, K, 32)) ||
+      (rc = make_map(&tb, w, 2 * F, K, 128))) {
     cudaFreeAsync(w, c->stream);
     return rc;
   }
@@ -2103,7 +2170,7 @@ int fp_op_gate_up_swiglu(fp_ctx* c, const void* x, const void* w_gate, const voi
   p.K = K;
   p.out = out;
   p.ldo = F;
-  launch_gemm<EPI_SWIGLU>(c, ta, tb, p, c->stream);
+  launch_gemm<EPI_SWIGLU>(c, ta, tb, p, c->stream, &ta32);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(w, c->stream));
   return FP_OK;
@@ -2125,7 +2192,9 @@ int fp_op_qkv_rope_kv(fp_ctx* c, const void* x, const void* w_qkv, void* q_out, 
   CK(cudaMemcpyAsync(w, w_qkv, (size_t)n * K * 2, cudaMemcpyDeviceToDevice, c->stream));
   CUtensorMap ta, tb;
   int rc;
-  if ((rc = make_map(&ta, x, M, K, 128)) || (rc = make_map(&tb, w, N, K, 128))) {
+  CUtensorMap ta32;
+  if ((rc = make_map(&ta, x, M, K, 128)) || (rc = make_map(&ta32, x, M, K, 32)) ||
+      (rc = make_map(&tb, w, N, K, 128))) {
     cudaFreeAsync(w, c->stream);
     return rc;
   }
@@ -2144,7 +2213,7 @@ int fp_op_qkv_rope_kv(fp_ctx* c, const void* x, const void* w_qkv, void* q_out, 
   p.page_size = c->page_size;
   p.n_kv_heads = kv_cols / 128;
   p.norm_eps = c->cfg.rms_eps;
-  launch_gemm<EPI_QKV>(c, ta, tb, p, c->stream);
+  launch_gemm<EPI_QKV>(c, ta, tb, p, c->stream, &ta32);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(w, c->stream));
   return FP_OK;

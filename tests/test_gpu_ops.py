@@ -165,9 +165,82 @@ def test_gemm_streamk(ctx, M, N, K, epi):
     assert err <= tol, (err, scale)
 
 
-@pytest.mark.parametrize("policy", [-1, 3])
+@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (1, 4096, 4096), (7, 512, 1024),
+                                   (42, 4096, 4096), (42, 6144, 4096), (64, 1024, 14336),
+                                   (100, 28672, 4096), (163, 4096, 14336), (200, 256, 4096),
+                                   (256, 4096, 4096), (33, 128256 // 256 * 256, 512)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_skinny(ctx, M, N, K, epi):
+    """Swap-AB skinny GEMM (policy 4; skinny.cuh): weight rows as the MMA M dimension, tokens as
+    N, equal (128-row slice, k-block) ranges per CTA, contributor-ordered reduction by each
+    256-column block's last contributor. Covers one-CTA launches (tiny U), slices split among
+    many CTAs (long K), CTAs spanning several slices (wide N), M = 1 ... 256 (three token-tile
+    instantiations). Within bf16 tolerance of fp32 and bit-identical run to run."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + N + K + epi)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    if epi == 1:
+        R = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    else:
+        R = torch.randn(M, N, device="cuda", dtype=torch.bfloat16, generator=g)
+    ref = A.float() @ B.float().t() + (R.float() if epi == 2 else 0.0)
+    outs = []
+    try:
+        _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, 4, 0))
+        for _ in range(2):
+            out = R.clone()
+            torch.cuda.synchronize()
+            _lib.check(ctx.lib.fp_op_gemm(ctx.h, epi, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                          M, N, K))
+            ctx.sync()
+            outs.append(out)
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+    assert torch.equal(outs[0], outs[1])
+    err = (outs[0].float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    tol = 1e-5 * scale * K ** 0.5 if epi == 1 else 2 ** -7 * scale + 1e-3
+    assert err <= tol, (err, scale)
+
+
+@pytest.mark.parametrize("M", [1, 42, 163, 256])
+def test_gemm_skinny_vs_tiled(ctx, M):
+    """The skinny plan and the tiled plans agree within bf16 rounding of one output (their K
+    summation orders differ)."""
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+
+    N, K = 4096, 4096
+    g = torch.Generator(device="cuda").manual_seed(M + 11)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    R = torch.randn(M, N, device="cuda", dtype=torch.bfloat16, generator=g)
+    got = {}
+    try:
+        for mx in (256, 0):  # forced skinny plan, then tiled plans only
+            _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, 4 if mx else -1, 0))
+            _lib.check(ctx.lib.fp_ctx_set_skinny_max(ctx.h, mx))
+            out = R.clone()
+            torch.cuda.synchronize()
+            _lib.check(ctx.lib.fp_op_gemm(ctx.h, 2, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                          M, N, K))
+            ctx.sync()
+            got[mx] = out.float()
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+        ctx.lib.fp_ctx_set_skinny_max(ctx.h, 128)
+    scale = got[0].abs().max().item()
+    assert (got[256] - got[0]).abs().max().item() <= 2 ** -7 * scale
+
+
+@pytest.mark.parametrize("policy", [-1, 3, 4])
 @pytest.mark.parametrize("M,F,K", [(1, 128, 64), (300, 512, 512), (4096, 1536, 512),
-                                   (77, 14336 // 4, 4096), (386, 14336, 4096)])
+                                   (77, 14336 // 4, 4096), (386, 14336, 4096), (163, 14336, 4096)])
 def test_gate_up_swiglu(ctx, M, F, K, policy):
     """gate_up GEMM + SwiGLU epilogue vs torch fp32: silu(x Wg^T) * (x Wu^T)."""
     import torch
@@ -193,9 +266,11 @@ def test_gate_up_swiglu(ctx, M, F, K, policy):
     assert err <= 2 ** -7 * ref.abs().max().item() + 1e-3, err
 
 
+@pytest.mark.parametrize("policy", [-1, 4])
 @pytest.mark.parametrize("M,q_cols,kv_cols,K", [(1, 512, 256, 512), (77, 512, 256, 512),
-                                                 (300, 4096, 1024, 1024), (700, 1024, 128, 256)])
-def test_qkv_rope_kv(ctx, M, q_cols, kv_cols, K):
+                                                 (300, 4096, 1024, 1024), (700, 1024, 128, 256),
+                                                 (42, 4096, 1024, 4096), (256, 1024, 256, 2048)])
+def test_qkv_rope_kv(ctx, M, q_cols, kv_cols, K, policy):
     """qkv_proj with its fused epilogue vs torch fp32: [q|k|v] = x W^T, rotate-half RoPE on q and
     k at arbitrary positions (the context's theta), K/V scattered into the paged layout."""
     import torch
@@ -215,10 +290,16 @@ def test_qkv_rope_kv(ctx, M, q_cols, kv_cols, K):
     q = torch.empty(M, q_cols, device="cuda", dtype=torch.bfloat16)
     kv = torch.zeros(n_pages, 2, hkv, ps, 128, device="cuda", dtype=torch.bfloat16)
     torch.cuda.synchronize()
-    _lib.check(ctx.lib.fp_op_qkv_rope_kv(ctx.h, x.data_ptr(), w.data_ptr(), q.data_ptr(),
-                                         kv.data_ptr(), pos_d.data_ptr(), tp_d.data_ptr(), M,
-                                         q_cols, kv_cols, K))
-    ctx.sync()
+    if policy == 4 and M > 256:
+        pytest.skip("skinny GEMM covers M <= 256")
+    try:
+        _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, policy, 0))
+        _lib.check(ctx.lib.fp_op_qkv_rope_kv(ctx.h, x.data_ptr(), w.data_ptr(), q.data_ptr(),
+                                             kv.data_ptr(), pos_d.data_ptr(), tp_d.data_ptr(), M,
+                                             q_cols, kv_cols, K))
+        ctx.sync()
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
     y = x.float() @ w.float().t()
     inv = theta ** (-torch.arange(64, dtype=torch.float64) * 2 / 128)
     ang = pos.double()[:, None] * inv[None, :]
