@@ -66,10 +66,10 @@ struct SkinnySum {
                                                        (long long)r * 128 + (colB & 127));
     const long long st4 = slot_elems / 4;
     const int n = max(ca, cb);
-    for (int s0 = 0; s0 < n; s0 += 2) {
-      float4 f[2][8];
+    for (int s0 = 0; s0 < n; s0 += ILP) {
+      float4 f[ILP][8];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < ILP; ++j) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -78,7 +78,7 @@ struct SkinnySum {
         }
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < ILP; ++j) {
         if (s0 + j < n) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
+  if (threadIdx.x == 0) GEMM_STAMP(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
     tma_prefetch(&tmW);
@@ -136,8 +137,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_STAMP(1);
   grid_dep_wait();
   const bool run = guard_block(p.guard);
+  if (threadIdx.x == 0) GEMM_STAMP(2);
 
   const int M = p.M;
   const int ntok = (M + 15) & ~15;   // MMA N
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], Cfg::W_BYTES + nbox * 4096);
+          if (i == 0 && kb == kb0) GEMM_STAMP(3);
           tma_load_2d_hint(sW + s * Cfg::W_BYTES, &tmW, &full[s], kb * kGemmBK, t * 128, pol_w);
           for (int b = 0; b < nbox; ++b)
             tma_load_2d_hint(sX + s * Cfg::X_BYTES + b * 4096, &tmX, &full[s], kb * kGemmBK,
@@ -192,6 +196,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (lane == 0 && i == 0 && kb == kb0) GEMM_STAMP(4);
         if (lane == 0) {
           const uint64_t a0 = make_sdesc_sw128(smem_u32(sW + s * Cfg::W_BYTES), 16, 1024);
           const uint64_t b0 = make_sdesc_sw128(smem_u32(sX + s * Cfg::X_BYTES), 16, 1024);
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       if (lane == 0) tc_commit(&tfull[acc]);
+      if (lane == 0 && i == n_seg - 1) GEMM_STAMP(5);
       __syncwarp();
     }
   } else if (warp >= 4) {
@@ -219,6 +225,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
+      if (row == 0 && i == 0) GEMM_STAMP(6);
       // partial -> slot (CTA g, slice t) = g + t: [token][128] fp32, each warp store is one
       // contiguous 128-byte row segment
       float* dst = p.ws + (long long)(blockIdx.x + t) * slot_elems + row;
@@ -236,20 +243,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (row == 0) GEMM_STAMP(7);
     if (n_seg > 0) {
       // Every partial of the launch is in the workspace once all CTAs arrive (the grid is at
       // most one CTA per SM, all resident: the next kernel launches only after every CTA has
       // issued its loads). Then the reduction + fused epilogue is spread over all warps of the
       // grid -- a single finisher per block is a serial L2-latency chain (~70 us at M = 256).
       int* ctr = p.tickets + 2048;  // [0] arrivals, [1] departures (zero between launches)
-      __threadfence();
+      // the CTA barrier orders the 128 drains before row 0's cumulative gpu-scope fence and
+      // arrival; its acquiring spin + the second barrier order everyone's loads after it
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (row == 0) {
+        __threadfence();
         atomicAdd(ctr, 1);
-        while (ld_acquire_gpu(ctr) < (int)gridDim.x) __nanosleep(32);
+        while (ld_acquire_gpu(ctr) < (int)gridDim.x) __nanosleep(20);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      __threadfence();
+      if (row == 0) GEMM_STAMP(8);
       // work group = 4 token rows x 8 items of one 256-column block (one warp; the 8 items of
       // a row are 8 consecutive lanes, as split_item_epilogue's shuffles require)
       const int gpb = (M + 3) >> 2;
@@ -272,6 +282,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       // the last CTA out re-arms the counters (every CTA has passed the arrival spin)
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (row == 0) GEMM_STAMP(9);
       if (row == 0 && atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
         ctr[0] = 0;
         ctr[1] = 0;
@@ -279,6 +290,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 0) GEMM_STAMP(10);
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
