@@ -181,6 +181,11 @@ DEVI AttnWork attn_decode(const AttnTcParams& p, int w) {
   return a;
 }
 
+// Registers: 10 warps put 3 warps on two of the four SM sub-partitions, whose 16K-register banks
+// cap a thread at 168 registers; ptxas stops there and spills 28 B (one loop-carried scalar per
+// KV tile, L1-resident). A __maxnreg__(200) build is spill-free at 193 registers but fails to
+// launch on the B200 ("too many resources requested", although 200 x 320 < 64K: the per-sub-
+// partition bank limit, 3 warps x 32 x regs <= 16384, is what binds).
 __global__ void __launch_bounds__(tcattn::THREADS, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                            const __grid_constant__ CUtensorMap tmKV,

@@ -30,7 +30,7 @@ struct XchgParams {
 
 // One warp per (row, 256-column segment): 32 lanes x 8 bf16 = the segment, so the fused
 // norm's segment sum of squares is one warp reduction.
-__global__ void __launch_bounds__(256) tp_allreduce_kernel(const XchgParams p) {
+__global__ void __launch_bounds__(256, 1) tp_allreduce_kernel(const XchgParams p) {
   __shared__ int s_xc;
   grid_dep_wait();
   if (!guard_block(p.guard)) return;
