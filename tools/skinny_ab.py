@@ -26,11 +26,13 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--hbm", type=float, default=7.7e12, help="HBM bytes/s for the bound")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--ops", default=",".join(SHAPES_NK), help="subset of " + ",".join(SHAPES_NK))
     a = ap.parse_args()
     ctx = PrefillContext(SHAPES["tiny"], kv_pages=8, max_pos=1024)
     st = torch.cuda.ExternalStream(ctx.stream_ptr)
     rows = []
-    for name, (N, K) in SHAPES_NK.items():
+    for name in a.ops.split(","):
+        N, K = SHAPES_NK[name]
         wbytes = N * K * 2
         ncopy = max(2, int(600e6 // wbytes) + 1)
         Bs = [torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * 0.05 for _ in range(ncopy)]
