@@ -192,12 +192,17 @@ def test_gemm_skinny(ctx, M, N, K, epi):
     try:
         _lib.check(ctx.lib.fp_ctx_set_gemm_policy(ctx.h, 4, 0))
         for _ in range(2):
-            out = R.clone()
+            # output inside a guard band of canary rows (an out-of-bounds write check: the
+            # compute-sanitizer is not available on the GPU pool)
+            band = torch.full((M + 16, N), 7.0, device="cuda", dtype=R.dtype)
+            band[8:8 + M] = R
+            out = band[8:8 + M]
             torch.cuda.synchronize()
             _lib.check(ctx.lib.fp_op_gemm(ctx.h, epi, A.data_ptr(), B.data_ptr(), out.data_ptr(),
                                           M, N, K))
             ctx.sync()
-            outs.append(out)
+            assert bool((band[:8] == 7.0).all()) and bool((band[8 + M:] == 7.0).all())
+            outs.append(out.clone())
     finally:
         ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
     assert torch.equal(outs[0], outs[1])
