@@ -327,9 +327,11 @@ __device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const S
     uint4 hv[4];  // residual loads in flight with the partial loads
     float ss = 0.f;
     if (valid) {
+      if (threadIdx.x == 128) GEMM_STAMP(12);
 #pragma unroll
       for (int i = 0; i < 4; ++i) hv[i] = ld_global_v4(hrow + 8 * i);
       sum.get(r, g * 32, g * 32 + 16, v);
+      if (threadIdx.x == 128) GEMM_STAMP(13);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t hw[4] = {hv[i].x, hv[i].y, hv[i].z, hv[i].w};
@@ -345,6 +347,7 @@ __device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const S
         const float rv = __bfloat162float(__float2bfloat16(v[i]));
         ss += rv * rv;
       }
+      if (threadIdx.x == 128) GEMM_STAMP(14);
       store_row32_bf16(hrow, v);
     }
     float tot = 0.f;  // chunks 0-3 and 4-7: the two 128-column segments of the tile
@@ -352,6 +355,7 @@ __device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const S
     for (int j = 0; j < 4; ++j) tot += __shfl_sync(0xffffffffu, ss, (lane & ~3) + j);
     if (valid && (g & 3) == 0 && p.ssq_out != nullptr)
       p.ssq_out[(long long)m * p.nseg + nb * 2 + (g >> 2)] = tot;
+    if (threadIdx.x == 128 && valid) GEMM_STAMP(15);
   } else if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32) {
     if (!valid) return;
     sum.get(r, g * 32, g * 32 + 16, v);
