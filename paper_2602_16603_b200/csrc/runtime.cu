@@ -227,6 +227,7 @@ struct fp_ctx {
   std::atomic<long long> launches{0};
   // split-K workspace (one prefill stream: launches are serialised, one buffer suffices)
   float* ws = nullptr;
+  long long ws_floats = 0;  // capacity of ws
   int* tickets = nullptr;
   int* attn_sched = nullptr;  // persistent attention work counter (self-resetting)
   unsigned long long* gemm_dbg = nullptr;  // FP_GEMM_STAMPS=1: phase stamps of fp_op_gemm launches
@@ -608,8 +609,7 @@ static bool launch_gemm_skinny(fp_ctx* c, const CUtensorMap* x32, const CUtensor
     return false;
   const long long U = (long long)(p.N / 128) * (p.K / kGemmBK);
   const int grid = (int)std::max(1LL, std::min<long long>(c->num_sms, U / 4));  // >= 4 k-blocks
-  const long long ws_floats = 8LL * c->num_sms * kGemmBM * 256;
-  if ((long long)(grid + p.N / 128) * p.M * 128 > ws_floats) return false;
+  if ((long long)(grid + p.N / 128) * p.M * 128 > c->ws_floats) return false;  // partial slots
   p.ws = c->ws;
   p.tickets = c->tickets;
   if (p.M <= 64) launch_skinny_t<EPI, 64>(c, *x32, w, p, grid, st);
@@ -1193,7 +1193,8 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
   }
   c->free_pages.resize(kv_pages);
   for (long long i = 0; i < kv_pages; ++i) c->free_pages[i] = (int)(kv_pages - 1 - i);
-  CK(cudaMalloc(&c->ws, (size_t)8 * c->num_sms * kGemmBM * 256 * sizeof(float)));
+  c->ws_floats = 8LL * c->num_sms * kGemmBM * 256;
+  CK(cudaMalloc(&c->ws, (size_t)c->ws_floats * sizeof(float)));
   CK(cudaMalloc(&c->attn_sched, 2 * sizeof(int)));
   CK(cudaMemset(c->attn_sched, 0, 2 * sizeof(int)));
   CK(cudaMalloc(&c->tickets, 4096 * sizeof(int)));
