@@ -204,6 +204,53 @@ struct GmemSum {
   }
 };
 
+// Sum provider of the split path: GmemSum's reduction, or the same over the K-slice CTAs of a
+// cluster (dsm): each CTA's fp32 partial then sits in its own shared memory as [col/4][row]
+// float4 (the layout of one GmemSum slice) and is read through distributed shared memory --
+// die-local, no L2 round trips (the L2 version's first item stalls ~4 us on partials just
+// written by other SMs). Summed in split order from 0 either way: the same bits.
+template <bool DSM>
+struct SplitSum {
+  const float4* ws_tile;  // L2 workspace of the tile (!DSM)
+  uint32_t sbase;         // this CTA's partial, shared::cta address (DSM)
+  int S;
+  template <int ILP = 4>
+  DEVI void get(int r, int colA, int colB, float* v) const {
+    if constexpr (!DSM) {
+      GmemSum{ws_tile, S}.template get<ILP>(r, colA, colB, v);
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    const uint32_t oa = (uint32_t)(((colA / 4) * kGemmBM + r) * 16);
+    const uint32_t ob = (uint32_t)(((colB / 4) * kGemmBM + r) * 16);
+    for (int s0 = 0; s0 < S; s0 += ILP) {
+      float4 f[ILP][8];
+#pragma unroll
+      for (int j = 0; j < ILP; ++j)
+        if (s0 + j < S) {
+          const uint32_t b = mapa_shared(sbase, (uint32_t)(s0 + j));
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            f[j][i] = ld_dsmem_f4(b + oa + i * kGemmBM * 16);
+            f[j][4 + i] = ld_dsmem_f4(b + ob + i * kGemmBM * 16);
+          }
+        }
+#pragma unroll
+      for (int j = 0; j < ILP; ++j)
+        if (s0 + j < S) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            v[4 * i] += f[j][i].x;
+            v[4 * i + 1] += f[j][i].y;
+            v[4 * i + 2] += f[j][i].z;
+            v[4 * i + 3] += f[j][i].w;
+          }
+        }
+    }
+  }
+};
+
 DEVI void store16_bf16(__nv_bfloat16* dst, const float* v) {
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -456,6 +503,9 @@ __device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const S
 
 // MODE 0: plain tiles. MODE 1: the instantiation that also runs tail split-K tiles (launched only
 // when the launcher chose splits > 1; MODE 0 carries no split code and no extra registers).
+// MODE 4: MODE 1 for launches whose tiles are ALL split, launched as clusters of the S K-slice
+// CTAs of each tile: the partials stay in each CTA's shared memory and are summed through
+// distributed shared memory (SplitSum<true>) between two cluster barriers.
 // MODE 2: grouped GEMM for MoE experts -- A rows are expert-ordered segments, the m-tile table
 // (expert, first row) and its length come from device memory (moe_plan_block), the B rows of
 // expert e start at e * grp_b_rows, rows past the expert's segment are masked, and the fused
@@ -807,12 +857,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
-      if (MODE == 1 && splits > 1) {
+      if ((MODE == 1 || MODE == 4) && splits > 1) {
         mbar_wait(&tfull[acc], acc_ph);
         if (threadIdx.x == 128) GEMM_STAMP(6);
         tc_fence_after();
-        // 1) this K-slice's partial tile -> workspace, TMEM released immediately
-        float4* dst = ws_tile + (long long)split * (BN / 4) * kGemmBM + row;
+        // 1) this K-slice's partial tile -> workspace, TMEM released immediately (cluster split:
+        //    -> this CTA's shared memory; the pipeline stages are free, all of its MMAs are done)
+        constexpr bool dsm = MODE == 4;
+        float4* dst = dsm ? reinterpret_cast<float4*>(smem) + row
+                          : ws_tile + (long long)split * (BN / 4) * kGemmBM + row;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -820,9 +873,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tmem_ld_wait();
           if (live) {  // dead rows (m >= M) are neither stored nor reduced
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              st_global_v4(dst + (c * 8 + i) * kGemmBM,
-                           make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]));
+            for (int i = 0; i < 8; ++i)  // generic store: global workspace or shared memory
+              *reinterpret_cast<uint4*>(dst + (c * 8 + i) * kGemmBM) =
+                  make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
           }
         }
         if (threadIdx.x == 128) GEMM_STAMP(7);
@@ -831,14 +884,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         //    spin: the launcher gives every CTA at most one split unit, as its last unit, and
         //    the grid never exceeds one CTA (pair) per SM, so all siblings are resident.
         int* tk = p.tickets + wtile;  // [0, 1024): arrivals, +1024: done
-        split_barrier(tk, splits);
+        if constexpr (dsm) {  // the tile's K-slice CTAs are this cluster (the other warps join)
+          cluster_arrive_release();
+          cluster_wait_acquire();
+        } else {
+          split_barrier(tk, splits);
+        }
         if (threadIdx.x == 128) GEMM_STAMP(8);
         // 3) this K-slice's share of the tile's (row, column-group) epilogue items, each the
         //    split-order sum of the partials (deterministic) -- the reduction is spread over
         //    all K-slice CTAs instead of one CTA reducing the whole tile
         const int m_base = row_a;
         const int live_rows = min(kGemmBM, p.M - m_base);
-        const GmemSum gsum{ws_tile, splits};
+        const SplitSum<dsm> gsum{ws_tile, smem_u32(smem), splits};
         // 8 items per row, row-major: a warp covers 4 whole rows
         const int items = live_rows * 8;
         for (int base = split * 128 + (row & ~31); base < items; base += splits * 128) {
@@ -847,7 +905,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           split_item_epilogue<EPI>(p, gsum, item < items, m_base + r, r, item & 7, n0, nb);
         }
         if (threadIdx.x == 128) GEMM_STAMP(9);
-        // 4) the last K-slice through resets the tickets for the next launch
+        // 4) the last K-slice through resets the tickets for the next launch (cluster split: the
+        //    peers' partials stay live until every K-slice has read them)
+        if constexpr (dsm) {
+          cluster_arrive_release();
+          cluster_wait_acquire();
+          continue;
+        }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (row == 0 && atomicAdd(tk + 1024, 1) == splits - 1) {
           tk[0] = 0;
@@ -874,7 +938,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if constexpr (EPI == EPI_RESID) {
         // residual row segment prefetched into registers while the MMA runs (MODE 1 loads it
         // per 32-column chunk instead: the split path's registers leave no room for 128 more)
-        constexpr bool kPrefetch = MODE != 1;
+        constexpr bool kPrefetch = MODE != 1 && MODE != 4;
         uint4 hres[kPrefetch ? BN / 8 : 1];
         __nv_bfloat16* hrow = p.resid + (long long)m * p.ldr + n0;
         if (kPrefetch && live) {
@@ -967,7 +1031,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int page = live ? p.tok_page[m] : 0;
         // (cos, sin) of the row's position for the 64 rotation pairs, prefetched during the MMA
         // (MODE 1 reads them per half at use: no room for 128 prefetched registers there)
-        constexpr bool kPrefetch = MODE != 1;
+        constexpr bool kPrefetch = MODE != 1 && MODE != 4;
         float4 cs[kPrefetch ? 32 : 1];
         const bool rot = n0 < p.q_cols + p.kv_cols;  // tile holds q/k heads (v heads unrotated)
         const float4* cs_src = reinterpret_cast<const float4*>(p.rope + (long long)pos * 64);
@@ -1083,6 +1147,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (EPI == EPI_STORE_BF16 && p.xchg) __threadfence_system();  // partials visible to peers
   }
 
+  if (MODE == 4 && run && warp < 4) {  // the cluster split's two barriers
+    cluster_arrive_release();
+    cluster_wait_acquire();
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  }
   if (threadIdx.x == 0) GEMM_STAMP(10);
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/arrivals are all done

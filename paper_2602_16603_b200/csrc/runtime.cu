@@ -249,6 +249,11 @@ struct fp_ctx {
   // Swap-AB skinny GEMM (skinny.cuh) for launches of at most skinny_max_m tokens
   // (FP_SKINNY_MAX_M / fp_ctx_set_skinny_max; 0 disables)
   int skinny_max_m = 128;
+  // Cluster split-K (gemm.cuh MODE 4): launches whose tiles are all split reduce inside a
+  // cluster through distributed shared memory (FP_SPLIT_DSMEM=0 disables). max_clusters[S] =
+  // co-resident clusters of S CTAs of the split kernel (occupancy query, cached; -1 unknown).
+  bool split_dsmem = true;
+  int max_clusters[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
   int sk_epoch = 0;         // per stream-K launch (flags compare against it: no reset)
 };
 
@@ -382,9 +387,13 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   once_per_device(attr, c->device, [] {
     cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI, CG, 0>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if constexpr (BN == 256)
+    if constexpr (BN == 256) {
       cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI, CG, 1>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+      if constexpr (CG == 1)
+        cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI, CG, 4>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    }
   });
   const int tiles = ((p.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * (p.N / BN);
   const int slots = c->num_sms / CG;  // concurrent tiles (CTA pairs)
@@ -436,6 +445,39 @@ static void launch_gemm_cg(fp_ctx* c, const CUtensorMap& a, const CUtensorMap& b
   cfg.numAttrs = 2;
   if constexpr (BN == 256) {
     if (p.splits > 1) {
+      // every tile split (short launches): the K-slices of a tile as one cluster, reduced in
+      // distributed shared memory -- when all the clusters are co-resident (one round)
+      if constexpr (CG == 1) {
+        if (c->split_dsmem && p.full_tiles == 0 && p.splits <= 8 && grid == units) {
+          int& mc = c->max_clusters[p.splits];
+          if (mc < 0) {
+            cudaLaunchConfig_t q = cfg;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = p.splits;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            q.gridDim = dim3(p.splits);
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tn_kernel<BN, EPI, CG, 4>, &q) !=
+                cudaSuccess) {
+              cudaGetLastError();
+              n = 0;
+            }
+            mc = n;
+            if (getenv("FP_DEBUG_PLAN"))
+              fprintf(stderr, "[fp] cluster split: %d co-resident clusters of %d CTAs\n", n,
+                      p.splits);
+          }
+          if (units / p.splits <= mc) {
+            attrs[1].val.clusterDim.x = p.splits;
+            cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 4>, a, b, p);
+            return;
+          }
+        }
+      }
       cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, EPI, CG, 1>, a, b, p);
       return;
     }
@@ -1184,6 +1226,7 @@ static int ctx_create_impl(int32_t device, const fp_model_cfg* cfg, int32_t tp_r
     if (const char* e = getenv("FP_FORCE_PAIR")) c->force_pair = atoi(e);
     if (const char* e = getenv("FP_TP_FUSED")) c->tp_fused = atoi(e) != 0;
     if (const char* e = getenv("FP_SKINNY_MAX_M")) c->skinny_max_m = atoi(e);
+    if (const char* e = getenv("FP_SPLIT_DSMEM")) c->split_dsmem = atoi(e) != 0;
     if (const char* e = getenv("FP_GEMM_STAMPS"))
       if (atoi(e)) CK(cudaMalloc(&c->gemm_dbg, (size_t)4096 * 16 * sizeof(unsigned long long)));
     const uint64_t rows = (uint64_t)L * kv_pages * 2 * c->hkv * page_size;

@@ -372,3 +372,53 @@ def _attn_ctx(shape):
     if "c" not in _ATTN:  # one context (weights are never touched by the op)
         _ATTN["c"] = PrefillContext(shape, kv_pages=64, page_size=128, max_pos=8192)
     return _ATTN["c"]
+
+
+@pytest.mark.parametrize("M,N,K,splits", [(42, 4096, 4096, 8), (42, 6144, 4096, 6),
+                                          (163, 4096, 14336, 4), (1, 256, 1024, 2),
+                                          (100, 1024, 4096, 8)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_split_cluster_matches_l2(ctx, M, N, K, splits, epi):
+    """Split-K with every tile split runs as clusters of the K-slice CTAs reducing through
+    distributed shared memory (gemm.cuh MODE 4); a context created with FP_SPLIT_DSMEM=0 reduces
+    the same partials through the L2 workspace. Both sum in split order from 0: bit-identical,
+    and within bf16 tolerance of fp32."""
+    import os
+
+    import torch
+
+    from paper_2602_16603_b200 import _lib
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    os.environ["FP_SPLIT_DSMEM"] = "0"
+    try:
+        ctx_l2 = PrefillContext(SHAPES["tiny"], kv_pages=8, max_pos=1024)
+    finally:
+        del os.environ["FP_SPLIT_DSMEM"]
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + splits + epi + 5)
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * 0.05
+    if epi == 1:
+        R = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    else:
+        R = torch.randn(M, N, device="cuda", dtype=torch.bfloat16, generator=g)
+    ref = A.float() @ B.float().t() + (R.float() if epi == 2 else 0.0)
+    outs = []
+    try:
+        for c in (ctx, ctx_l2):
+            _lib.check(c.lib.fp_ctx_set_gemm_policy(c.h, 0, splits))
+            out = R.clone()
+            torch.cuda.synchronize()
+            _lib.check(c.lib.fp_op_gemm(c.h, epi, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                        M, N, K))
+            c.sync()
+            outs.append(out)
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+        ctx_l2.close()
+    assert torch.equal(outs[0], outs[1])
+    err = (outs[0].float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    tol = 1e-5 * scale * K ** 0.5 if epi == 1 else 2 ** -7 * scale + 1e-3
+    assert err <= tol, (err, scale)
