@@ -375,10 +375,25 @@ __device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const S
     float ss = 0.f;
     if (valid) {
       if (threadIdx.x == 128) GEMM_STAMP(12);
+#ifdef FP_GEMM_STAMPS
+      // diagnostic builds time the two dependencies apart: partials (13), then the residual
+      // row (14, forced by a use of every loaded word)
+      sum.get(r, g * 32, g * 32 + 16, v);
+      if (threadIdx.x == 128) GEMM_STAMP(13);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hv[i] = ld_global_v4(hrow + 8 * i);
+      if (threadIdx.x == 128) {
+        unsigned acc = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc ^= hv[i].x ^ hv[i].y ^ hv[i].z ^ hv[i].w;
+        if (acc == 0x12345678u) v[0] += 1e-30f;
+        GEMM_STAMP(14);
+      }
+#else
 #pragma unroll
       for (int i = 0; i < 4; ++i) hv[i] = ld_global_v4(hrow + 8 * i);
       sum.get(r, g * 32, g * 32 + 16, v);
-      if (threadIdx.x == 128) GEMM_STAMP(13);
+#endif
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t hw[4] = {hv[i].x, hv[i].y, hv[i].z, hv[i].w};
@@ -394,7 +409,6 @@ __device__ __forceinline__ void split_item_epilogue(const GemmParams& p, const S
         const float rv = __bfloat162float(__float2bfloat16(v[i]));
         ss += rv * rv;
       }
-      if (threadIdx.x == 128) GEMM_STAMP(14);
       store_row32_bf16(hrow, v);
     }
     float tot = 0.f;  // chunks 0-3 and 4-7: the two 128-column segments of the tile
@@ -897,10 +911,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int m_base = row_a;
         const int live_rows = min(kGemmBM, p.M - m_base);
         const SplitSum<dsm> gsum{ws_tile, smem_u32(smem), splits};
-        // 8 items per row, row-major: a warp covers 4 whole rows
+        // 8 items per row, row-major: a warp covers 4 whole rows. Warp groups of 32 items are
+        // dealt to the K-slice CTAs first (group gi -> slice gi % S, warp gi / S % 4), so a
+        // short tile's reduction reads spread over all S SMs instead of the first few (the
+        // reads are per-SM bandwidth bound: tools/gemm_stamps.py it_start -> it_sum)
         const int items = live_rows * 8;
-        for (int base = split * 128 + (row & ~31); base < items; base += splits * 128) {
-          const int item = base + lane;
+        for (int gi = q * splits + split; gi * 32 < items; gi += 4 * splits) {
+          const int item = gi * 32 + lane;
           const int r = item >> 3;
           split_item_epilogue<EPI>(p, gsum, item < items, m_base + r, r, item & 7, n0, nb);
         }

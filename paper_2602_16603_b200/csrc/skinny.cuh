@@ -264,7 +264,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // a row are 8 consecutive lanes, as split_item_epilogue's shuffles require)
       const int gpb = (M + 3) >> 2;
       const int total = (p.N / 256) * gpb;
-      for (int gi = (int)blockIdx.x * 4 + q; gi < total; gi += (int)gridDim.x * 4) {
+      // groups dealt to the CTAs first (gi -> CTA gi % G, warp gi / G): the reads are per-SM
+      // bandwidth bound, so a short launch spreads them over every SM
+      for (int gi = q * (int)gridDim.x + (int)blockIdx.x; gi < total; gi += (int)gridDim.x * 4) {
         const int nb = gi / gpb;
         const int item = (gi - nb * gpb) * 32 + lane;
         const int r = item >> 3;

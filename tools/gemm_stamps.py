@@ -15,7 +15,7 @@ from paper_2602_16603_b200.config import SHAPES  # noqa: E402
 from paper_2602_16603_b200.native import PrefillContext  # noqa: E402
 
 NAMES = ["entry", "prolog", "guard", "tma0", "mma0", "commit", "epi", "stored", "splitbar",
-         "items", "exit", "teardown", "it_start", "it_sum", "it_add", "it_done"]
+         "items", "exit", "teardown", "it_start", "it_sum", "it_resid", "it_done"]
 
 
 def main():
