@@ -16,7 +16,7 @@ def short(name):
     m = re.search(r"gemm_bf16_tn_kernel<(?:\(int\))?(\d+), *(?:\(int\))?(\d+), *(?:\(int\))?(\d+)(?:, *(?:\(bool\))?(\w+))?>", name)
     if m:
         mode = {"1": " split-capable", "true": " split-capable", "2": " grouped(MoE)",
-                "3": " stream-K"}.get(m.group(4), "")
+                "3": " stream-K", "4": " cluster-split"}.get(m.group(4), "")
         width = "" if m.group(1) == "256" else f" {m.group(1)}-wide"
         return f"gemm {epi.get(m.group(2), m.group(2))} cta_group={m.group(3)}{width}{mode}"
     for k in ("attn_prefill_tc_kernel", "rmsnorm_kernel", "init_normal_kernel"):
