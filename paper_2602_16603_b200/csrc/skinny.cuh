@@ -7,9 +7,9 @@
 //
 // Realises the same reference entries as gemm.cuh (prefillsim/cost_model.py:38-44, 234-242:
 // qkv_proj / o_proj / gate_up_proj / down_proj of a chunk with few concatenated tokens, plus the
-// lm_head at one row per request). Short requests are weight-streaming bound (a Llama-3-8B layer
-// is 435 MB of weights against 2 * 42 * 218 MFLOP at 42 tokens), so the launch is planned for
-// HBM: the (128-row weight slice, 64-wide k-block) space is cut into one equal contiguous range
+// lm_head at one row per request). Short launches are weight-streaming bound (a Llama-3-8B layer
+// streams 435 MB of weights, ~56 us at 7.7 TB/s, for 18 GFLOP at 42 tokens, ~13 us at
+// 1.4 PFLOP/s), so the launch is planned for HBM: the (128-row weight slice, 64-wide k-block) space is cut into one equal contiguous range
 // per CTA, stream-K fashion, so all SMs pull weights for the whole launch with no wave
 // quantisation. Each CTA's range covers a few "segments" (one weight slice, a k-block range);
 // each segment's fp32 partial goes to its own workspace slot ([token][128 cols], coalesced
@@ -18,6 +18,9 @@
 // deterministic, the same bits on every run -- and runs the fused epilogue of gemm.cuh
 // (split_item_epilogue: residual + segment sums of squares, SwiGLU, QKV + RoPE + paged KV
 // scatter, fp32 logits).
+//
+// The auto plan (runtime.cu launch_gemm_skinny) takes it where the B200 A/B shows it ahead of
+// the tiled plans: a few rows (M <= 8: lm_head, tiny chunks) and long-K launches up to 128 rows.
 //
 // Layout of one CTA (256 threads, 1 CTA / SM): warp 0 TMA producer (weight box 128 x 64 with an
 // evict-first hint: streamed once; token boxes 32 x 64, evict-last: re-read by every CTA),
