@@ -202,6 +202,79 @@ def test_forced_gemm_tiling_vs_oracle(tiny, policy):
         P.kv(f"{name} V[{r}]", v, ot.v_cache[r][shape.num_layers - 1])
 
 
+@pytest.mark.parametrize("chunk", [None, 96, 200])
+def test_skinny_gemm_forward_vs_oracle(tiny, chunk):
+    """Every GEMM launch of at most 256 rows on the swap-AB skinny kernel (policy 4): with
+    chunks of 96 / 200 tokens that is every qkv / o / gate_up / down launch of the forward (fused
+    input norm, RoPE + paged KV scatter, SwiGLU, residual + sums of squares through the skinny
+    kernel's grid-wide reduction), unchunked only the lm_head; logits and KV within tolerance of
+    the oracle, and bit-identical run to run."""
+    shape, w, ctx = tiny
+    tokens = F.make_tokens([37, 300, 130], shape.vocab, 23)
+    ot = F.OracleTask(shape, w, tokens, chunk)
+    ot.run_all()
+    runs = []
+    try:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, 4, 0)
+        for _ in range(2):
+            t = run_straight(ctx, tokens, chunk)
+            runs.append((t.logits(), [t.read_kv(r, shape.num_layers - 1) for r in range(3)]))
+            t.destroy()
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+    (lg, kv), (lg2, kv2) = runs
+    assert np.array_equal(lg, lg2)
+    for (k, v), (k2, v2) in zip(kv, kv2):
+        assert np.array_equal(k, k2) and np.array_equal(v, v2)
+    name = f"tiny skinny gemm chunk {chunk}"
+    P.logits(name, lg, ot.logits)
+    for r, (k, v) in enumerate(kv):
+        P.kv(f"{name} K[{r}]", k, ot.k_cache[r][shape.num_layers - 1])
+        P.kv(f"{name} V[{r}]", v, ot.v_cache[r][shape.num_layers - 1])
+
+
+@pytest.mark.parametrize("splits", [2, 4, 8])
+def test_cluster_split_forward_bitexact(tiny, splits):
+    """A chunked forward with every GEMM tile split into K-slices (forced): the all-split
+    launches reduce inside clusters through distributed shared memory (gemm.cuh MODE 4); a
+    context created with FP_SPLIT_DSMEM=0 reduces through the L2 workspace. Logits and KV are
+    bit-identical between the two and within tolerance of the oracle."""
+    import os
+
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    shape, w, ctx = tiny
+    os.environ["FP_SPLIT_DSMEM"] = "0"
+    try:
+        ctx_l2 = PrefillContext(SHAPES["tiny"], kv_pages=64, page_size=128, max_pos=8192)
+    finally:
+        del os.environ["FP_SPLIT_DSMEM"]
+    tokens = F.make_tokens([37, 300, 130], shape.vocab, 29)
+    out = []
+    try:
+        ctx_l2.load_weights(w)
+        for c in (ctx, ctx_l2):
+            c.lib.fp_ctx_set_gemm_policy(c.h, 0, splits)
+            t = run_straight(c, tokens, 96)
+            out.append((t.logits(), [t.read_kv(r, shape.num_layers - 1) for r in range(3)]))
+            t.destroy()
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+        ctx_l2.close()
+    (lg, kv), (lg2, kv2) = out
+    assert np.array_equal(lg, lg2)
+    for (k, v), (k2, v2) in zip(kv, kv2):
+        assert np.array_equal(k, k2) and np.array_equal(v, v2)
+    ot = F.OracleTask(shape, w, tokens, 96)
+    ot.run_all()
+    name = f"tiny cluster split S={splits}"
+    P.logits(name, lg, ot.logits)
+    for r, (k, v) in enumerate(kv):
+        P.kv(f"{name} K[{r}]", k, ot.k_cache[r][shape.num_layers - 1])
+        P.kv(f"{name} V[{r}]", v, ot.v_cache[r][shape.num_layers - 1])
+
+
 def test_page_pool_exhaustion_is_clean():
     """A task that needs more KV pages than are free fails with the pool untouched, and the
     context keeps working (fp_task_create releases everything it took on any failure)."""
