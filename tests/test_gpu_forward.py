@@ -149,10 +149,12 @@ def test_preemption_bitwise_and_cursor(tiny, gran):
     t.destroy()
 
 
+@pytest.mark.parametrize("policy", [-1, 4])
 @pytest.mark.parametrize("name", ["tiny-qwen3", "tiny-qwen2"])
-def test_qwen_variants_vs_hf_and_oracle(golden_dir, name):
+def test_qwen_variants_vs_hf_and_oracle(golden_dir, name, policy):
     """Qwen3 q/k-norm and Qwen2.5 QKV bias in the fused QKV epilogue; vocab 8000 (not a
-    multiple of 256: lm_head padded internally)."""
+    multiple of 256: lm_head padded internally). Policy 4 runs every launch (chunks of 96) on
+    the swap-AB skinny kernel, whose reduction feeds the same epilogues."""
     from paper_2602_16603_b200.config import SHAPES
     from paper_2602_16603_b200.native import PrefillContext
 
@@ -160,19 +162,20 @@ def test_qwen_variants_vs_hf_and_oracle(golden_dir, name):
     w = F.make_weights(shape, 1234)
     ctx = PrefillContext(SHAPES[name], kv_pages=64, max_pos=4096)
     ctx.load_weights(w)
+    ctx.lib.fp_ctx_set_gemm_policy(ctx.h, policy, 0)
     g = np.load(f"{golden_dir}/{name}_hf_logits.npz")
     tokens = F.make_tokens(list(g["lens"]), shape.vocab, int(g["seed"]))
     t = run_straight(ctx, tokens, 96)
     lg = t.logits()
     assert lg.shape == (len(tokens), 8000)
-    P.logits(f"{name} vs HF golden", lg, g["logits"])
+    P.logits(f"{name} (gemm policy {policy}) vs HF golden", lg, g["logits"])
     ot = F.OracleTask(shape, w, tokens, 96)
     ot.run_all()
-    P.logits(f"{name} vs oracle", lg, ot.logits)
+    P.logits(f"{name} (gemm policy {policy}) vs oracle", lg, ot.logits)
     for r in range(len(tokens)):
         k, v = t.read_kv(r, 1)
-        P.kv(f"{name} K[{r}][1]", k, ot.k_cache[r][1])
-        P.kv(f"{name} V[{r}][1]", v, ot.v_cache[r][1])
+        P.kv(f"{name} (policy {policy}) K[{r}][1]", k, ot.k_cache[r][1])
+        P.kv(f"{name} (policy {policy}) V[{r}][1]", v, ot.v_cache[r][1])
     t.destroy()
     ctx.close()
 

@@ -65,10 +65,21 @@ def test_golden_hf_qwen3_moe(moe, golden_dir):
     t.destroy()
 
 
-@pytest.mark.parametrize("lens,chunk", [([300], None), ([37, 130, 64, 201], None),
-                                        ([37, 130, 64, 201], 100), ([1000, 5], 256)])
-def test_moe_logits_kv_routing_vs_oracle(moe, lens, chunk):
+@pytest.mark.parametrize("lens,chunk,policy", [([300], None, -1), ([37, 130, 64, 201], None, -1),
+                                               ([37, 130, 64, 201], 100, -1), ([1000, 5], 256, -1),
+                                               ([37, 130, 64, 201], 100, 4)])
+def test_moe_logits_kv_routing_vs_oracle(moe, lens, chunk, policy):
+    """Policy 4: the router (fp32 logits with the fused post-attention norm) and the qkv / o
+    launches on the swap-AB skinny kernel; the grouped expert GEMMs are unchanged."""
     shape, w, ctx = moe
+    ctx.lib.fp_ctx_set_gemm_policy(ctx.h, policy, 0)
+    try:
+        _moe_vs_oracle(shape, w, ctx, lens, chunk, policy)
+    finally:
+        ctx.lib.fp_ctx_set_gemm_policy(ctx.h, -1, 0)
+
+
+def _moe_vs_oracle(shape, w, ctx, lens, chunk, policy):
     tokens = F.make_tokens(lens, shape.vocab, 77)
     ot = F.OracleTask(shape, w, tokens, chunk)
     t = ctx.create_task(tokens, chunk, "operator")
@@ -81,7 +92,7 @@ def test_moe_logits_kv_routing_vs_oracle(moe, lens, chunk):
     ctx.sync()
     assert t.poll().state == 3
     ot.run_all()
-    name = f"tiny-moe lens={lens} chunk={chunk}"
+    name = f"tiny-moe lens={lens} chunk={chunk}" + (f" gemm policy {policy}" if policy >= 0 else "")
     P.logits(name, t.logits(), ot.logits)
     for r in range(len(lens)):
         for layer in (0, shape.num_layers - 1):
