@@ -217,3 +217,38 @@ def test_llama_layer_dims_chunked_vs_oracle(chunk, lens):
         t.destroy()
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("chunk,lens,policy", [(128, [300, 42], 4), (256, [300, 42], 4),
+                                               (128, [300, 42], -1)])
+def test_llama_layer_dims_short_launches_vs_oracle(chunk, lens, policy):
+    """Short launches at the Llama-3-8B layer dimensions (2 layers): chunks of 128 / 256 tokens
+    with every GEMM forced onto the swap-AB skinny kernel (policy 4: K = 4096 / 14336, N = 6144 /
+    4096 / 28672, one token tile of 48-256 columns) and, for comparison, the auto plans (split-K,
+    cluster split-K, skinny down_proj); logits and KV within the stated tolerance of the oracle."""
+    from dataclasses import replace
+
+    from oracle import forward as F
+    from paper_2602_16603_b200.config import SHAPES
+    from paper_2602_16603_b200.native import PrefillContext
+
+    oshape = F.Shape(2, 4096, 32, 8, 128, 14336, 8192, 5e5)
+    w = F.make_weights(oshape, 9)
+    gshape = replace(SHAPES["llama3-8b"], num_layers=2, vocab=8192)
+    c = PrefillContext(gshape, kv_pages=64, page_size=128, max_pos=8192)
+    try:
+        c.load_weights(w)
+        c.lib.fp_ctx_set_gemm_policy(c.h, policy, 0)
+        tokens = F.make_tokens(lens, oshape.vocab, 6)
+        ot = F.OracleTask(oshape, w, tokens, chunk)
+        ot.run_all()
+        t = run(c, tokens, chunk)
+        name = f"llama3-8b dims 2L chunk {chunk} gemm policy {policy}"
+        P.logits(name, t.logits(), ot.logits)
+        for i in range(2):
+            k, v = t.read_kv(i, 1)
+            P.kv(f"{name} K[{i}][1]", k, ot.k_cache[i][1])
+            P.kv(f"{name} V[{i}][1]", v, ot.v_cache[i][1])
+        t.destroy()
+    finally:
+        c.close()
